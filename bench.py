@@ -1,0 +1,384 @@
+"""Benchmark of the convolution-only deconvolution hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Metric (BASELINE.json): voxel-iterations/s of the projected-gradient iteration (forward
+full conv + residual + adjoint valid correlation + projected update + reductions).
+A "step" is one PG iteration over one batch: config 2 = 16 independent 2048x2048
+images, 31x31 Gaussian PSF (sigma 4), Poisson noise at peak 1000.  Inputs are seeded
+synthetic data of exactly that shape (no dataset exists); they are resident in HBM
+before the timed region and, at 16 x 2048^2 fp32 (>= 268 MB per tensor), larger than
+the 126 MB L2, so no flush is needed between steps.
+
+One JSON line on rank 0.  `value` is device time (CUDA events on the plan's stream,
+max over ranks); `e2e` is the same metric through the public C-ABI call with host f64
+buffers (H2D of Y, power-iteration step estimate, all iterations, D2H of the estimate
+and traces inside the timed region); `roofline` is the dominant kernel's algorithmic
+FLOP rate against the FP32 FFMA peak; `cpu_baseline` is the reference (oracle/_ref,
+the unmodified reference compiled from /root/reference) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_SM = 148
+FFMA_PER_SM_CLK = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    return ap.parse_args()
+
+
+# --- distributed plumbing -------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Dist:
+    def __init__(self, backend="nccl"):
+        self.rank, self.world, self.local = dist_env()
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist = dist
+            self.torch = torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# --- clocks sampler -----------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [s.strip() for s in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --- inputs -----------------------------------------------------------------------------------
+
+def inputs(config: str, rank: int):
+    from paper_1711_11224_b200 import synth
+    x, y, h = synth.make(config, seed=synth.SEED + 100003 * rank)
+    if x.ndim == len(h.shape):  # single volume -> batch of one
+        x, y = x[None], y[None]
+    return x.astype(np.float32), y.astype(np.float32), h
+
+
+def algorithmic(config: str, batch: int, x_shape, h):
+    K = int(np.prod(h.shape))
+    voxels = batch * int(np.prod(x_shape))
+    y_vox = batch * int(np.prod([a + b - 1 for a, b in zip(x_shape, h.shape)]))
+    rho = y_vox / voxels
+    return K, voxels, rho
+
+
+# --- CPU baseline (reference compiled from /root/reference: oracle/_ref) --------------------
+
+def cpu_reference_sample(config: str, iters: int, warm: int = 0):
+    """Time `iters` PG iterations of the reference's own operators (ref_pg_iterations,
+    solvers.hpp:179-228 loop body) on ONE image of the config, all host threads."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "c")
+    cores = os.cpu_count() or 1
+    orc.set_threads(cores)
+    from paper_1711_11224_b200 import synth
+    if config in ("c1", "c2"):
+        x, y, h = synth.make(config, batch=1) if config == "c2" else (None, None, None)
+        if config == "c2":
+            y = y[0]
+            xs = (2048, 2048)
+        else:
+            x, y, h = synth.make("c1")
+            xs = x.shape
+        sample = f"1 image {xs[0]}x{xs[1]}, PSF {h.shape}"
+    else:
+        # reduced xy crop of the 3D configs with the same PSF
+        shape = {"c3": (128, 256, 256), "c4": (64, 128, 128), "c5": (64, 96, 96)}[config]
+        x, y, h = synth.make(config, shape=shape, n_objects=200)
+        xs = x.shape
+        sample = f"volume {xs}, PSF {h.shape}"
+    step0 = 1.0  # unit-sum PSFs: lambda_max(A^T A) <= 1; the loop body cost is step-independent
+    if kind == "reference":
+        aty = orc.adjoint_apply(y, h, xs)
+        xk = np.maximum(aty, 0.0)
+        ax = orc.conv_full(xk, h)
+        f = 0.5 * float(np.sum((ax - y) ** 2))
+        if warm:
+            f, _ = orc.pg_iterations(y, h, xs, step0, warm, xk, ax, aty, f)
+        t0 = time.perf_counter()
+        f, acc = orc.pg_iterations(y, h, xs, step0, iters, xk, ax, aty, f)
+        dt = time.perf_counter() - t0
+    else:
+        t0 = time.perf_counter()
+        orc.deconv_pg(y, h, xs, max_iters=iters, tol_rel_objective=0.0, initial_step=step0)
+        dt = time.perf_counter() - t0
+    vox = int(np.prod(xs))
+    return {"value": vox * iters / dt, "unit": "voxel-iterations/s", "cores": cores, "kind": kind,
+            "sample": f"{sample}, {iters} PG iterations (loop body only), {dt:.2f} s"}, dt
+
+
+# --- our arm ------------------------------------------------------------------------------------
+
+def run_ours(a):
+    rank, world, local = dist_env()
+    d = Dist("nccl")
+    import torch  # plumbing only: external-stream CUDA events and the rank collectives
+    from paper_1711_11224_b200 import ndconv as nd
+    if nd.device_count() < 1:
+        raise SystemExit("no B200 visible")
+    x, y, h = inputs(a.config, rank)
+    B = y.shape[0]
+    x_shape = x.shape[1:]
+    K, voxels, rho = algorithmic(a.config, B, x_shape, h)
+    cfg = nd.DeconvConfig(max_iters=a.warmup + a.steps + 1, tol_rel_objective=0.0)
+
+    plan = nd.Plan(x_shape, h, batch=B, device=local)
+    plan.set_observation(y)
+    plan.pg_begin(cfg)
+    for _ in range(a.warmup):
+        plan.pg_iterate(1)
+    torch.cuda.set_device(local)
+    stream = torch.cuda.ExternalStream(plan.stream(), device=f"cuda:{local}")
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    plan.reset_stats()
+    plan.set_timing(True)
+    clocks = Clocks(local)
+    clocks.start()
+    d.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        plan.pg_iterate(1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_max = d.max(ms)
+    n_fwd, ms_fwd = plan.stats(0)
+    n_adj, ms_adj = plan.stats(1)
+    n_all, _ = plan.stats(2)
+    plan.set_timing(False)
+    plan.pg_end()
+    rep = plan.report(0, cfg.max_iters + 1)
+    plan.close()
+
+    value = world * voxels * a.steps / (ms_max / 1e3)
+    # dominant kernel roofline: algorithmic FLOPs per launch = 2 K per x voxel (forward:
+    # every x voxel meets K taps; adjoint: every output meets K taps)
+    flops_launch = 2.0 * K * voxels
+    dom, n_dom, ms_dom = ("adjoint", n_adj, ms_adj) if ms_adj >= ms_fwd else ("forward", n_fwd, ms_fwd)
+    avg_s = ms_dom / max(n_dom, 1) / 1e3
+    achieved = flops_launch / avg_s / 1e12
+    smax = clk.get("sm_max_mhz") or 1965.0
+    peak = N_SM * FFMA_PER_SM_CLK * 2 * smax * 1e6 / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(a.config, {}).get(dom)
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
+        "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{a.config}: 16x2048x2048 2D batch, PSF 31x31 sigma 4, Poisson 1000"
+                   if a.config == "c2" else a.config,
+                   "batch_per_gpu": B, "x_shape": list(x_shape), "psf": list(h.shape), "taps": K,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (no flush)", "step": "one PG iteration over the batch",
+                   "tol_rel_objective": 0.0, "step_size": "auto (power iteration, untimed setup)"},
+        "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_basis": f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (sm max clock); "
+                                   "no measured FP32 peak in MEASURED_PEAKS.json",
+                     "algorithmic_flops_per_launch": flops_launch,
+                     "launch_ms": avg_s * 1e3,
+                     "frac_at_observed_clock": (achieved / (N_SM * FFMA_PER_SM_CLK * 2 * clk["sm_mhz"] * 1e6 / 1e12)
+                                                if clk.get("sm_mhz") else None),
+                     "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}},
+        "gpu_launches": int(n_all),
+        "clocks": clk,
+        "iterations_accepted": int(rep.iterations_run),
+        "backtracks": int(rep.extra.get("backtracks", 0)),
+    }
+    if not a.no_e2e:
+        line["e2e"] = e2e(a, nd, y, h, x_shape, B, voxels, world, d)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cb, _ = cpu_reference_sample(a.config, a.cpu_iters)
+        line["cpu_baseline"] = cb
+    d.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e(a, nd, y32, h, x_shape, B, voxels, world, d):
+    """Public C-ABI call (ndc_deconv_pg_batch_f64) with host f64 buffers: the whole
+    config-2 solve (auto step, 100 iterations) per step, copies included."""
+    import ctypes as C
+    from paper_1711_11224_b200 import _native as N
+    iters = 100 if a.config == "c2" else 20
+    yh = np.ascontiguousarray(y32, dtype=np.float64)
+    xo = np.empty((B,) + tuple(x_shape), np.float64)
+    cap = iters + 1
+    obj = np.empty((B, cap))
+    kkt = np.empty((B, cap))
+    reps = (N.Report * B)()
+    cfg = nd.DeconvConfig(max_iters=iters, tol_rel_objective=0.0).to_c()
+    ext = (C.c_size_t * len(x_shape))(*x_shape)
+    yext = (C.c_size_t * len(x_shape))(*yh.shape[1:])
+    hext = (C.c_size_t * h.ndim)(*h.shape)
+    hh = np.ascontiguousarray(h, np.float64)
+
+    def call():
+        rc = N.lib().ndc_deconv_pg_batch_f64(B, h.ndim, yext, yh.ctypes.data_as(N.dbl_p), hext,
+                                             hh.ctypes.data_as(N.dbl_p), ext, C.byref(cfg),
+                                             xo.ctypes.data_as(N.dbl_p), obj.ctypes.data_as(N.dbl_p),
+                                             kkt.ctypes.data_as(N.dbl_p), cap, reps)
+        if rc:
+            raise RuntimeError(N.lib().ndc_last_error().decode())
+
+    call()  # warm-up (module load, allocator)
+    reps_t = []
+    for _ in range(2):
+        d.barrier()
+        t0 = time.perf_counter()
+        call()
+        reps_t.append(time.perf_counter() - t0)
+    dt = d.max(min(reps_t))
+    return {"value": world * voxels * iters / dt, "unit": "voxel-iterations/s",
+            "h2d_bytes_per_step": int(yh.nbytes + hh.nbytes), "d2h_bytes_per_step": int(xo.nbytes + obj.nbytes + kkt.nbytes),
+            "step": f"one full deconv_pg_batch_f64 call: {B} images, {iters} iterations, auto step",
+            "seconds_per_step": dt}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cb = None
+    times = []
+    warm_total = 0.0
+    for i in range(a.warmup + a.steps):
+        cb, dt = cpu_reference_sample(a.config, 1)
+        if i >= a.warmup:
+            times.append(dt)
+        else:
+            warm_total += dt
+    per = float(np.sum(times))
+    vox = 2048 * 2048 if a.config == "c2" else None
+    value = cb["value"] if vox is None else vox * a.steps / per
+    cb = dict(cb, value=value, sample=cb["sample"].rsplit(",", 1)[0] + f", {a.steps} timed steps of 1 PG iteration")
+    line = {
+        "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
+        "impl": "reference", "value": value, "unit": "voxel-iterations/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": per / a.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{a.config} (reference CPU path, 1 image per step)", "parallelism": "cpu threads"},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

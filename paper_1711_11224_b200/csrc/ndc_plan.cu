@@ -1,0 +1,755 @@
+// Host side of the hot path: buffers, launch geometry, and the projected-gradient
+// driver that restates ndconv::deconv_pg (solvers.hpp:155-238) with device-resident
+// tensors.  See ndc_plan.h for the contract and DESIGN.md for the data layout.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "ndc_plan.h"
+
+namespace ndc {
+
+namespace {
+// Device scalar slots (doubles), per image unless noted.
+enum Slot { kF = 0, kKKT = 1, kCHG = 2, kAUX = 3, kNumSlots = 4 };
+constexpr int kMaxPowerIters = 4096;
+constexpr int kElemBlocks = 148 * 4;  // elementwise kernels: blocks per image
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+}  // namespace
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? NDC_ERR_NO_DEVICE : NDC_ERR_CUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+Vol Vol::make(int z, int y, int x) {
+  Vol v;
+  v.ez = z;
+  v.ey = y;
+  v.ex = x;
+  v.pitch = cdiv(x, kTileX) * kTileX;
+  v.plane = v.pitch * y;
+  v.image = v.plane * z;
+  return v;
+}
+
+Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t* k_ext,
+           const double* h, std::unique_ptr<Transport> comm)
+    : device_(device), B_(batch), ndim_(ndim), comm_(std::move(comm)) {
+  if (ndim < 1 || ndim > 3)
+    fail(ndim < 1 ? NDC_ERR_SHAPE : NDC_ERR_UNSUPPORTED,
+         "ndconv_b200: the device path handles 1- to 3-d tensors, got " + std::to_string(ndim));
+  if (batch == 0) fail(NDC_ERR_ARGUMENT, "ndconv_b200: batch must be positive");
+  size_t count = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (x_ext[i] == 0) fail(NDC_ERR_SHAPE, "Shape: extents must be positive");
+    if (k_ext[i] == 0) fail(NDC_ERR_SHAPE, "Shape: extents must be positive");
+    if (k_ext[i] % 2 == 0) fail(NDC_ERR_SHAPE, "Kernel: extents must be odd");
+    count *= k_ext[i];
+  }
+  for (size_t i = 0; i < count; ++i)
+    if (!std::isfinite(h[i])) fail(NDC_ERR_NUMERIC, "Kernel: values must be finite");
+  const int lead = 3 - ndim;
+  for (int i = 0; i < ndim; ++i) {
+    xext_[lead + i] = x_ext[i];
+    kext_[lead + i] = k_ext[i];
+  }
+  mz_ = static_cast<int>(xext_[0]);
+  my_ = static_cast<int>(xext_[1]);
+  mx_ = static_cast<int>(xext_[2]);
+  KZ_ = static_cast<int>(kext_[0]);
+  KY_ = static_cast<int>(kext_[1]);
+  KX_ = static_cast<int>(kext_[2]);
+  pz_ = (KZ_ - 1) / 2;
+  py_ = (KY_ - 1) / 2;
+  px_ = (KX_ - 1) / 2;
+  if (KX_ > kMaxKX)
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: kernel x-extent " + std::to_string(KX_) + " > " +
+                                  std::to_string(kMaxKX));
+  if (kTileY + KY_ - 1 > kMaxRows)
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: kernel y-extent " + std::to_string(KY_) + " too large");
+  if (KY_ * KX_ > kTapCap)
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: one kernel z-slice exceeds the per-launch tap block");
+  if (static_cast<long long>(my_) + 2 * py_ > (1 << 30) || static_cast<long long>(mx_) + 2 * px_ > (1 << 30))
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: extent too large");
+
+  // Taps: adjoint correlates with h, forward with flip(h) (kernel.hpp:41-45).
+  taps_adj_.resize(count);
+  taps_fwd_.resize(count);
+  kernel_all_zero_ = true;
+  for (size_t i = 0; i < count; ++i) {
+    taps_adj_[i] = static_cast<float>(h[i]);
+    taps_fwd_[count - 1 - i] = static_cast<float>(h[i]);
+    if (h[i] != 0.0) kernel_all_zero_ = false;
+  }
+
+  // z-slab geometry: rank r owns x planes [xa, xb) and y planes
+  // [xa+pz, xb+pz) (the first rank also [0, pz), the last up to mz+2pz).
+  if (comm_) {
+    rank_ = comm_->rank();
+    world_ = comm_->world();
+    if (B_ != 1) fail(NDC_ERR_ARGUMENT, "ndconv_b200: sharded plans hold one image");
+  }
+  size_t a, b, ya, yb;
+  ndc_slab_range(static_cast<size_t>(mz_), static_cast<size_t>(pz_), rank_, world_, &a, &b, &ya, &yb);
+  xa_ = static_cast<int>(a);
+  xb_ = static_cast<int>(b);
+  xa_n_ = xb_ - xa_;
+  ya_ = static_cast<int>(ya);
+  yb_ = static_cast<int>(yb);
+  if (world_ > 1 && xa_n_ < pz_)
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: z-slab of " + std::to_string(xa_n_) +
+                                  " planes is thinner than the halo (" + std::to_string(pz_) + ")");
+  xlo_ = std::max(0, xa_ - pz_);
+  xhi_ = std::min(mz_, xb_ + pz_);
+  rlo_ = xa_;
+  rhi_ = xb_ + 2 * pz_;
+  if (world_ == 1) {
+    xlo_ = 0;
+    xhi_ = mz_;
+  }
+  X_ = Vol::make(xhi_ - xlo_, my_, mx_);
+  Y_ = Vol::make(rhi_ - rlo_, my_ + 2 * py_, mx_ + 2 * px_);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(NDC_ERR_NO_DEVICE, "ndconv_b200: no CUDA device (the device path has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev) fail(NDC_ERR_ARGUMENT, "ndconv_b200: bad device ordinal");
+  check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceProp prop;
+  check_cuda(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    fail(NDC_ERR_NO_DEVICE, std::string("ndconv_b200: built for sm_100a, device is ") + prop.name);
+  check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  alloc_all();
+}
+
+Plan::~Plan() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& e : ev_pool_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (void* p : {static_cast<void*>(x_), static_cast<void*>(trial_), static_cast<void*>(g_),
+                  static_cast<void*>(yobs_), static_cast<void*>(r_), static_cast<void*>(rt_),
+                  static_cast<void*>(scratch_), static_cast<void*>(partials_),
+                  static_cast<void*>(dsc_), static_cast<void*>(dscale_),
+                  static_cast<void*>(dactive_), static_cast<void*>(dstep_), static_cast<void*>(gather_),
+                  staging_})
+    if (p) cudaFree(p);
+  if (hsc_) cudaFreeHost(hsc_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+float* Plan::dev_alloc_f(long long n) {
+  void* p = nullptr;
+  check_cuda(cudaMalloc(&p, static_cast<size_t>(n) * 4), "cudaMalloc");
+  check_cuda(cudaMemsetAsync(p, 0, static_cast<size_t>(n) * 4, stream_), "cudaMemset");
+  return static_cast<float*>(p);
+}
+
+long long Plan::partials_per_image(Dir d) const {
+  const Vol& vo = (d == kFwd) ? Y_ : X_;
+  const long long nz = (d == kFwd) ? (yb_ - ya_) : (xb_ - xa_);
+  return nz * cdiv(vo.ex, kTileX) * cdiv(vo.ey, kTileY);
+}
+
+void Plan::alloc_all() {
+  const long long nx = X_.image * static_cast<long long>(B_);
+  const long long ny = Y_.image * static_cast<long long>(B_);
+  x_ = dev_alloc_f(nx);
+  trial_ = dev_alloc_f(nx);
+  g_ = dev_alloc_f(nx);
+  yobs_ = dev_alloc_f(ny);
+  r_ = dev_alloc_f(ny);
+  rt_ = dev_alloc_f(ny);
+  const int slices_per = kTapCap / (KY_ * KX_);
+  if (KZ_ > slices_per) scratch_ = dev_alloc_f(std::max(nx, ny));
+  partials_cap_ = static_cast<long long>(B_) *
+                  std::max({partials_per_image(kFwd), partials_per_image(kAdj),
+                            static_cast<long long>(kElemBlocks)});
+  check_cuda(cudaMalloc(&partials_, partials_cap_ * sizeof(double2)), "cudaMalloc partials");
+  const size_t nsc = kNumSlots * B_ + kMaxPowerIters + 16;
+  check_cuda(cudaMalloc(&dsc_, nsc * sizeof(double)), "cudaMalloc scalars");
+  check_cuda(cudaMemsetAsync(dsc_, 0, nsc * sizeof(double), stream_), "cudaMemset");
+  check_cuda(cudaMallocHost(&hsc_, nsc * sizeof(double)), "cudaMallocHost");
+  check_cuda(cudaMalloc(&dscale_, B_ * sizeof(float)), "cudaMalloc scale");
+  check_cuda(cudaMalloc(&dactive_, B_ * sizeof(int)), "cudaMalloc active");
+  check_cuda(cudaMalloc(&dstep_, B_ * sizeof(double)), "cudaMalloc step");
+  if (world_ > 1) check_cuda(cudaMalloc(&gather_, 2 * world_ * sizeof(double)), "cudaMalloc gather");
+  std::vector<float> ones(B_, 1.0f);
+  check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+  std::vector<int> act(B_, 1);
+  check_cuda(cudaMemcpyAsync(dactive_, act.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+  staging_bytes_ = static_cast<size_t>(std::max(X_.ez * static_cast<long long>(X_.ey) * X_.ex,
+                                                Y_.ez * static_cast<long long>(Y_.ey) * Y_.ex)) * 8;
+  check_cuda(cudaMalloc(&staging_, staging_bytes_), "cudaMalloc staging");
+  sync();
+}
+
+void Plan::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+
+const CUtensorMap& Plan::map_for(const float* base, Dir d) {
+  auto key = std::make_pair(base, static_cast<int>(d));
+  auto it = maps_.find(key);
+  if (it != maps_.end()) return it->second;
+  const Vol& v = (d == kFwd) ? X_ : Y_;
+  CUtensorMap m;
+  const CUresult rc = encode_tensor_map(&m, base, v.ex, v.ey, static_cast<long long>(v.ez) * B_,
+                                        v.pitch, v.plane, shared_pitch_for(KX_), kTileY + KY_ - 1);
+  if (rc != CUDA_SUCCESS)
+    fail(NDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
+  return maps_.emplace(key, m).first->second;
+}
+
+void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_out,
+                     const float* aux_in, const float* scale, const double* step, const int* active,
+                     bool partials) {
+  const bool fwd = d == kFwd;
+  const Vol& vin = fwd ? X_ : Y_;
+  const Vol& vout = fwd ? Y_ : X_;
+  const std::vector<float>& taps = fwd ? taps_fwd_ : taps_adj_;
+  CorrGeom g{};
+  g.in_ez = vin.ez;
+  g.in_ey = vin.ey;
+  g.in_ex = vin.ex;
+  g.out_ey = vout.ey;
+  g.out_ex = vout.ex;
+  int nz_out;
+  if (fwd) {
+    nz_out = yb_ - ya_;
+    g.out_z0 = ya_ - rlo_;
+    g.off_z = ya_ - 2 * pz_ - xlo_;
+    g.off_y = -2 * py_;
+    g.off_x = -2 * px_;
+  } else {
+    nz_out = xb_ - xa_;
+    g.out_z0 = xa_ - xlo_;
+    g.off_z = xa_ - rlo_;
+    g.off_y = 0;
+    g.off_x = 0;
+  }
+  g.KY = KY_;
+  g.tiles_x = static_cast<int>(cdiv(vout.ex, kTileX));
+  g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY));
+  g.rows = kTileY + KY_ - 1;
+  g.pitch_s = shared_pitch_for(KX_);
+  g.out_pitch = vout.pitch;
+  g.out_plane = vout.plane;
+  g.out_image = vout.image;
+  g.mode = mode;
+  const int per_slice = KY_ * KX_;
+  const int slices_per = kTapCap / per_slice;
+  const int nchunks = static_cast<int>(cdiv(KZ_, slices_per));
+  const CUtensorMap& map = map_for(in, d);
+  static thread_local TapBlock tb;
+  for (int c = 0; c < nchunks; ++c) {
+    g.kz0 = c * slices_per;
+    g.kz1 = std::min(KZ_, g.kz0 + slices_per);
+    g.stages = std::min(2, g.kz1 - g.kz0);
+    g.accum = c > 0;
+    g.final_chunk = (c == nchunks - 1);
+    CorrArgs a{};
+    a.out = g.final_chunk ? out : scratch_;
+    a.accum_in = scratch_;
+    a.aux_out = aux_out;
+    a.aux_in = aux_in;
+    a.scale = scale;
+    a.step = step;
+    a.active = active;
+    a.partials = (g.final_chunk && partials) ? partials_ : nullptr;
+    std::memcpy(tb.t, taps.data() + static_cast<size_t>(g.kz0) * per_slice,
+                static_cast<size_t>(g.kz1 - g.kz0) * per_slice * sizeof(float));
+    size_t ev = 0;
+    if (timing_) {
+      if (ev_used_ == ev_pool_.size()) {
+        cudaEvent_t e0, e1;
+        check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
+        check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+        ev_pool_.emplace_back(e0, e1);
+      }
+      ev = ev_used_++;
+      check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
+    }
+    check_cuda(launch_correlate(KX_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
+               "correlate launch");
+    if (timing_) {
+      check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
+      ev_pending_.emplace_back(fwd ? 0 : 1, ev);
+    }
+    st_[fwd ? 0 : 1].launches++;
+    st_[2].launches++;
+  }
+}
+
+void Plan::drain_events() {
+  if (ev_pending_.empty()) return;
+  sync();
+  for (auto& pe : ev_pending_) {
+    float ms = 0.f;
+    check_cuda(cudaEventElapsedTime(&ms, ev_pool_[pe.second].first, ev_pool_[pe.second].second),
+               "cudaEventElapsedTime");
+    st_[pe.first].ms += ms;
+  }
+  ev_pending_.clear();
+  ev_used_ = 0;
+}
+
+void Plan::reset_stats() {
+  drain_events();
+  for (auto& s : st_) s = KernelStats{};
+}
+
+KernelStats Plan::stats(int kind) {
+  drain_events();
+  if (kind < 0 || kind > 2) fail(NDC_ERR_ARGUMENT, "stats kind");
+  return st_[kind];
+}
+
+void Plan::finalize(long long per_image, int op, double* out0, double* out1, float* scale_out,
+                    const int* active) {
+  if (world_ == 1) {
+    check_cuda(launch_finalize(partials_, per_image, static_cast<int>(B_), op, out0, out1, scale_out,
+                               active, stream_),
+               "finalize launch");
+    st_[2].launches++;
+    return;
+  }
+  // z-slab ranks: raw local reduction -> all-gather (rank order) -> identical combine.
+  const int raw = (op == kFinMaxSum) ? kFinMaxSum : kFinSumSum;
+  double* gin = dsc_ + kNumSlots * B_ + kMaxPowerIters;  // 2 doubles
+  double* gout = gather_;                                 // 2 * world doubles
+  check_cuda(launch_finalize(partials_, per_image, 1, raw, gin, gin + 1, nullptr, active, stream_),
+             "finalize launch");
+  comm_->allgather(gin, gout, 2, stream_);
+  check_cuda(launch_combine(gout, world_, op, out0, out1, scale_out, stream_), "combine launch");
+  st_[2].launches += 2;
+}
+
+// Halo planes: the forward pass needs p_z x-planes from each neighbour,
+// the adjoint p_z y-planes; slabs are at least p_z thick so one neighbour suffices.
+void Plan::halo_x(float* buf) {
+  if (world_ == 1 || pz_ == 0) return;
+  const size_t n = static_cast<size_t>(pz_) * X_.plane;
+  auto at = [&](int global_plane) { return buf + static_cast<long long>(global_plane - xlo_) * X_.plane; };
+  const bool lo = rank_ > 0, hi = rank_ + 1 < world_;
+  comm_->exchange(lo ? at(xa_) : nullptr, lo ? at(xa_ - pz_) : nullptr, hi ? at(xb_ - pz_) : nullptr,
+                  hi ? at(xb_) : nullptr, n, stream_);
+}
+
+void Plan::halo_y(float* buf) {
+  if (world_ == 1 || pz_ == 0) return;
+  const size_t n = static_cast<size_t>(pz_) * Y_.plane;
+  auto at = [&](int global_plane) { return buf + static_cast<long long>(global_plane - rlo_) * Y_.plane; };
+  const bool lo = rank_ > 0, hi = rank_ + 1 < world_;
+  comm_->exchange(lo ? at(xa_ + pz_) : nullptr, lo ? at(xa_) : nullptr, hi ? at(xb_) : nullptr,
+                  hi ? at(xb_ + pz_) : nullptr, n, stream_);
+}
+
+void Plan::upload_active(const std::vector<int>& act) {
+  check_cuda(cudaMemcpyAsync(dactive_, act.data(), act.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             stream_),
+             "H2D active");
+  sync();  // act lives on the host stack of the caller
+}
+
+// ---- host <-> device packing (dense row-major host, pitched device) -----------------
+void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz) {
+  const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  for (size_t b = 0; b < B_; ++b) {
+    check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 8, cudaMemcpyHostToDevice, stream_),
+               "H2D");
+    check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
+                               dev + b * v.image + static_cast<long long>(z_off) * v.plane, 1, nz,
+                               v.ey, v.ex, v.pitch, stream_),
+               "pack");
+    st_[2].launches++;
+  }
+  sync();
+}
+
+void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz) {
+  const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  for (size_t b = 0; b < B_; ++b) {
+    check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 4, cudaMemcpyHostToDevice, stream_),
+               "H2D");
+    check_cuda(launch_pack_f32(static_cast<const float*>(staging_),
+                               dev + b * v.image + static_cast<long long>(z_off) * v.plane, 1, nz,
+                               v.ey, v.ex, v.pitch, stream_),
+               "pack");
+    st_[2].launches++;
+  }
+  sync();
+}
+
+void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz) {
+  const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  for (size_t b = 0; b < B_; ++b) {
+    check_cuda(launch_unpack_f64(dev + b * v.image + static_cast<long long>(z_off) * v.plane,
+                                 static_cast<double*>(staging_), 1, nz, v.ey, v.ex, v.pitch, stream_),
+               "unpack");
+    st_[2].launches++;
+    check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 8, cudaMemcpyDeviceToHost, stream_),
+               "D2H");
+    sync();
+  }
+}
+
+void Plan::unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_off, int nz) {
+  const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  for (size_t b = 0; b < B_; ++b) {
+    check_cuda(launch_unpack_f32(dev + b * v.image + static_cast<long long>(z_off) * v.plane,
+                                 static_cast<float*>(staging_), 1, nz, v.ey, v.ex, v.pitch, stream_),
+               "unpack");
+    st_[2].launches++;
+    check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 4, cudaMemcpyDeviceToHost, stream_),
+               "D2H");
+    sync();
+  }
+}
+
+void Plan::set_observation_f64(const double* y) {
+  pack_dense_f64(y, yobs_, Y_, ya_ - rlo_, yb_ - ya_);
+  halo_y(yobs_);
+}
+void Plan::set_observation_f32(const float* y) {
+  pack_dense_f32(y, yobs_, Y_, ya_ - rlo_, yb_ - ya_);
+  halo_y(yobs_);
+}
+void Plan::set_x_f64(const double* x) {
+  pack_dense_f64(x, x_, X_, xa_ - xlo_, xa_n_);
+  halo_x(x_);
+}
+void Plan::get_estimate_f64(double* x) { unpack_dense_f64(x_, x, X_, xa_ - xlo_, xa_n_); }
+void Plan::get_estimate_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
+void Plan::get_y_buffer_f64(double* y) { unpack_dense_f64(r_, y, Y_, ya_ - rlo_, yb_ - ya_); }
+void Plan::get_x_buffer_f64(double* x, int which) {
+  unpack_dense_f64(which == 0 ? x_ : g_, x, X_, xa_ - xlo_, xa_n_);
+}
+
+// ---- operators ------------------------------------------------------------------------
+void Plan::op_conv_full() {
+  correlate(kFwd, x_, r_, kEpiStore, nullptr, nullptr, nullptr, nullptr, nullptr, false);
+}
+
+void Plan::op_adjoint_of_y() {
+  correlate(kAdj, yobs_, x_, kEpiStore, nullptr, nullptr, nullptr, nullptr, nullptr, false);
+}
+
+double Plan::op_objective() {
+  correlate(kFwd, x_, r_, kEpiResid, nullptr, yobs_, nullptr, nullptr, nullptr, true);
+  finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kF * B_, nullptr, nullptr, nullptr);
+  check_cuda(cudaMemcpyAsync(hsc_, dsc_ + kF * B_, B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  sync();
+  return hsc_[0];
+}
+
+void Plan::op_normal_gradient() {
+  op_objective();
+  halo_y(r_);
+  correlate(kAdj, r_, g_, kEpiStore, nullptr, nullptr, nullptr, nullptr, nullptr, false);
+}
+
+double Plan::op_kkt_residual() {
+  op_objective();
+  halo_y(r_);
+  correlate(kAdj, r_, nullptr, kEpiKKT, nullptr, x_, nullptr, nullptr, nullptr, true);
+  finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
+           nullptr);
+  check_cuda(cudaMemcpyAsync(hsc_, dsc_ + kKKT * B_, B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  sync();
+  return hsc_[0];
+}
+
+// solvers.hpp:127-143.  Run on image 0 only (the estimate depends on (h, shape) alone,
+// so every image of a batch shares it); v_i = w_{i-1}/lambda_{i-1} is folded into the
+// next forward pass as an output scale read on the device, so the 2*iters passes run
+// without a host round trip.
+double Plan::estimate_step(size_t power_iters) {
+  if (power_iters == 0) fail(NDC_ERR_CONFIG, "estimate_step: power_iters must be positive");
+  if (power_iters > static_cast<size_t>(kMaxPowerIters))
+    fail(NDC_ERR_UNSUPPORTED, "estimate_step: power_iters too large");
+  if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "estimate_step: degenerate all-zero kernel");
+  const double n = static_cast<double>(mz_) * my_ * mx_;
+  const size_t saveB = B_;
+  // image 0 only: launch with batch 1 (buffers are laid out image-major)
+  B_ = 1;
+  try {
+    const float one = 1.0f;
+    check_cuda(cudaMemcpyAsync(dscale_, &one, 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    check_cuda(launch_fill(x_owned(g_), static_cast<float>(1.0 / std::sqrt(n)), 1, xa_n_, my_, mx_,
+                           X_.pitch, stream_),
+               "fill");
+    st_[2].launches++;
+    double* lam = dsc_ + kNumSlots * saveB;
+    for (size_t i = 0; i < power_iters; ++i) {
+      halo_x(g_);
+      correlate(kFwd, g_, rt_, kEpiStore, nullptr, nullptr, dscale_, nullptr, nullptr, false);
+      halo_y(rt_);
+      correlate(kAdj, rt_, g_, kEpiNorm, nullptr, nullptr, nullptr, nullptr, nullptr, true);
+      finalize(partials_per_image(kAdj), kFinNorm, lam + i, nullptr, dscale_, nullptr);
+    }
+    check_cuda(cudaMemcpyAsync(hsc_, lam, power_iters * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+  } catch (...) {
+    B_ = saveB;
+    throw;
+  }
+  B_ = saveB;
+  maps_.clear();  // maps were encoded with zcount for batch 1
+  for (size_t i = 0; i < power_iters; ++i)
+    if (!(hsc_[i] > 0.0) || !std::isfinite(hsc_[i]))
+      fail(NDC_ERR_NUMERIC, "estimate_step: degenerate convolution operator");
+  // restore the per-image scale to 1 for later kEpiStore users
+  std::vector<float> ones(B_, 1.0f);
+  check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+  sync();
+  return 1.0 / hsc_[power_iters - 1];
+}
+
+// ---- projected gradient ---------------------------------------------------------------
+void Plan::pg_begin(const ndc_deconv_config& c) {
+  // solvers.hpp:65-76
+  if (c.max_iters == 0) fail(NDC_ERR_CONFIG, "DeconvConfig: max_iters must be positive");
+  if (!(c.tol_rel_objective >= 0)) fail(NDC_ERR_CONFIG, "DeconvConfig: tol_rel_objective must be >= 0");
+  if (c.has_initial_step && !(c.initial_step > 0))
+    fail(NDC_ERR_CONFIG, "DeconvConfig: initial_step must be positive");
+  if (!(c.backtrack_factor > 0) || !(c.backtrack_factor < 1))
+    fail(NDC_ERR_CONFIG, "DeconvConfig: backtrack_factor must be in (0,1)");
+  if (c.max_backtracks == 0) fail(NDC_ERR_CONFIG, "DeconvConfig: max_backtracks must be positive");
+  if (c.power_iters == 0) fail(NDC_ERR_CONFIG, "DeconvConfig: power_iters must be positive");
+  if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "deconv_pg: degenerate all-zero kernel");
+  cfg_ = c;
+  wall0_ = now_s();
+  step0_ = c.has_initial_step ? c.initial_step : estimate_step(c.power_iters);
+
+  img_.assign(B_, Img{});
+  std::vector<int> act(B_, 1);
+  upload_active(act);
+  // x0 = max(A^T y, 0) (solvers.hpp:166-167); A x0 and f (168-172)
+  correlate(kAdj, yobs_, x_, kEpiClamp, nullptr, nullptr, nullptr, nullptr, nullptr, false);
+  halo_x(x_);
+  correlate(kFwd, x_, r_, kEpiResid, nullptr, yobs_, nullptr, nullptr, nullptr, true);
+  finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kF * B_, nullptr, nullptr, nullptr);
+  check_cuda(cudaMemcpyAsync(hsc_, dsc_ + kF * B_, B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  std::vector<double> steps(B_, step0_);
+  check_cuda(cudaMemcpyAsync(dstep_, steps.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+  sync();
+  for (size_t b = 0; b < B_; ++b) {
+    img_[b].f = hsc_[b];
+    img_[b].obj.push_back(hsc_[b]);
+    img_[b].step = step0_;
+  }
+  halo_y(r_);
+  pg_begun_ = true;
+}
+
+size_t Plan::pg_iterate(size_t n) {
+  if (!pg_begun_) fail(NDC_ERR_ARGUMENT, "pg_iterate before pg_begin");
+  size_t active_count = 0;
+  for (size_t step = 0; step < n; ++step) {
+    std::vector<int> act(B_, 0);
+    active_count = 0;
+    for (size_t b = 0; b < B_; ++b) {
+      Img& im = img_[b];
+      if (im.active && im.kkt.size() >= cfg_.max_iters) im.active = false;  // max_iters
+      act[b] = im.active ? 1 : 0;
+      active_count += act[b];
+    }
+    if (active_count == 0) break;
+    upload_active(act);
+    std::vector<double> steps(B_, step0_);
+    check_cuda(cudaMemcpyAsync(dstep_, steps.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+
+    // g = A^T(A x - y) with kkt, trial = max(x - step0 g, 0), changed count (180-191)
+    correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, dactive_, true);
+    finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
+             dactive_);
+    halo_x(trial_);
+    // A trial, residual, f_trial (195-197)
+    correlate(kFwd, trial_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, dactive_, true);
+    finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kAUX * B_, nullptr, nullptr, dactive_);
+    check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+
+    // per-image decision (191-205)
+    enum { kAccept, kFixed, kBacktrack, kStall };
+    std::vector<int> state(B_, -1);
+    std::vector<double> ft(B_, 0.0), stp(B_, step0_);
+    std::vector<size_t> nbt(B_, 0);
+    for (size_t b = 0; b < B_; ++b) {
+      if (!act[b]) continue;
+      img_[b].kkt.push_back(hsc_[kKKT * B_ + b]);
+      const double chg = hsc_[kCHG * B_ + b];
+      ft[b] = hsc_[kAUX * B_ + b];
+      if (chg == 0.0)
+        state[b] = kFixed;
+      else if (ft[b] < img_[b].f)
+        state[b] = kAccept;
+      else
+        state[b] = kBacktrack;
+    }
+    // backtracking: step *= factor, up to max_backtracks more trials (189, 205)
+    for (;;) {
+      std::vector<int> bt(B_, 0);
+      size_t nb = 0;
+      for (size_t b = 0; b < B_; ++b) {
+        if (state[b] != kBacktrack) continue;
+        if (nbt[b] + 1 > cfg_.max_backtracks) {
+          state[b] = kStall;
+          continue;
+        }
+        nbt[b]++;
+        img_[b].backtracks++;
+        stp[b] *= cfg_.backtrack_factor;
+        bt[b] = 1;
+        nb++;
+      }
+      if (nb == 0) break;
+      upload_active(bt);
+      check_cuda(cudaMemcpyAsync(dstep_, stp.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+      check_cuda(launch_pg_trial(x_owned(x_), x_owned(g_), x_owned(trial_), dstep_, dactive_, partials_,
+                                 static_cast<int>(B_), 0, xa_n_, my_, mx_, X_.pitch, kElemBlocks,
+                                 stream_),
+                 "pg_trial launch");
+      st_[2].launches++;
+      finalize(kElemBlocks, kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr, dactive_);
+      halo_x(trial_);
+      correlate(kFwd, trial_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, dactive_, true);
+      finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kAUX * B_, nullptr, nullptr, dactive_);
+      check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_),
+                 "D2H");
+      sync();
+      for (size_t b = 0; b < B_; ++b) {
+        if (!bt[b]) continue;
+        ft[b] = hsc_[kAUX * B_ + b];
+        if (hsc_[kCHG * B_ + b] == 0.0)
+          state[b] = kFixed;
+        else if (ft[b] < img_[b].f)
+          state[b] = kAccept;
+      }
+    }
+    // commit (208-227)
+    bool any_accept = false;
+    for (size_t b = 0; b < B_; ++b) {
+      if (!act[b]) continue;
+      Img& im = img_[b];
+      if (state[b] == kFixed) {
+        im.reason = NDC_STOP_CONVERGED;
+        im.active = false;
+      } else if (state[b] == kStall) {
+        im.reason = NDC_STOP_STALLED;
+        im.active = false;
+      } else {
+        any_accept = true;
+        const double drop = im.f - ft[b];
+        im.f = ft[b];
+        im.obj.push_back(ft[b]);
+        im.iters = im.kkt.size();
+        if (drop <= cfg_.tol_rel_objective * im.obj[im.obj.size() - 2]) {
+          im.reason = NDC_STOP_CONVERGED;
+          im.active = false;
+        }
+      }
+    }
+    if (any_accept) {
+      std::swap(x_, trial_);
+      std::swap(r_, rt_);
+      // images that did not accept (stopped now or earlier) keep their previous iterate
+      for (size_t b = 0; b < B_; ++b)
+        if (state[b] != kAccept) {
+          copy_image_x(x_, trial_, b);
+          copy_image_y(r_, rt_, b);
+        }
+      halo_y(r_);
+    }
+  }
+  active_count = 0;
+  for (auto& im : img_)
+    if (im.active && im.kkt.size() < cfg_.max_iters) active_count++;
+  return active_count;
+}
+
+void Plan::copy_image_x(float* dst, const float* src, size_t b) {
+  check_cuda(cudaMemcpyAsync(dst + b * X_.image, src + b * X_.image, X_.image * 4,
+                             cudaMemcpyDeviceToDevice, stream_),
+             "D2D");
+}
+void Plan::copy_image_y(float* dst, const float* src, size_t b) {
+  check_cuda(cudaMemcpyAsync(dst + b * Y_.image, src + b * Y_.image, Y_.image * 4,
+                             cudaMemcpyDeviceToDevice, stream_),
+             "D2D");
+}
+
+void Plan::pg_end() {
+  if (!pg_begun_) fail(NDC_ERR_ARGUMENT, "pg_end before pg_begin");
+  // solvers.hpp:230-233: one more adjoint for images whose last iterate has no KKT.
+  std::vector<int> need(B_, 0);
+  size_t nneed = 0;
+  for (size_t b = 0; b < B_; ++b)
+    if (img_[b].kkt.size() < img_[b].obj.size()) {
+      need[b] = 1;
+      nneed++;
+    }
+  if (nneed) {
+    upload_active(need);
+    correlate(kAdj, r_, nullptr, kEpiKKT, nullptr, x_, nullptr, nullptr, dactive_, true);
+    finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
+             dactive_);
+    check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+    for (size_t b = 0; b < B_; ++b)
+      if (need[b]) img_[b].kkt.push_back(hsc_[kKKT * B_ + b]);
+  }
+  std::vector<int> all(B_, 1);
+  upload_active(all);
+  wall_ = now_s() - wall0_;
+  pg_begun_ = false;
+}
+
+void Plan::get_report(size_t image, ndc_deconv_report* rep, double* obj, double* kkt,
+                      size_t cap) const {
+  if (image >= img_.size()) fail(NDC_ERR_ARGUMENT, "report: image index out of range");
+  const Img& im = img_[image];
+  if (cap < im.obj.size() || cap < im.kkt.size())
+    fail(NDC_ERR_ARGUMENT, "report: trace capacity too small");
+  rep->iterations_run = im.iters;
+  rep->stop_reason = im.reason;
+  rep->wall_time_seconds = wall_;
+  rep->negative_pixels_clamped = im.clamped;
+  rep->trace_len = im.obj.size();
+  rep->backtracks = im.backtracks;
+  rep->step0 = step0_;
+  if (obj) std::memcpy(obj, im.obj.data(), im.obj.size() * 8);
+  if (kkt) std::memcpy(kkt, im.kkt.data(), im.kkt.size() * 8);
+}
+
+void Plan::bench_forward() {
+  correlate(kFwd, x_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, nullptr, true);
+}
+void Plan::bench_adjoint() {
+  correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, nullptr, true);
+}
+
+// ---- Richardson-Lucy (solvers.hpp:245-305) ----------------------------------------------
+void Plan::rl_run(const ndc_rl_config& c) {
+  (void)c;
+  fail(NDC_ERR_UNSUPPORTED, "deconv_rl: not wired in this build");
+}
+
+}  // namespace ndc

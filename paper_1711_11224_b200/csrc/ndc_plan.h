@@ -1,0 +1,191 @@
+// Plan: device buffers, operators and the projected-gradient driver for one
+// (x shape, kernel, batch) problem on one GPU -- or one z-slab of it on one rank.
+//
+// Mirrors ndconv::deconv_pg (solvers.hpp:155-238) with all tensors resident in HBM.
+// Per iteration and image the host sees only a handful of f64 scalars (objective,
+// KKT, changed-count) read back in one small D2H; the accept / backtrack / stop logic
+// is the reference's, evaluated per image.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ndc_internal.h"
+#include "../../include/ndconv_b200.h"
+
+namespace ndc {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+
+// Pitched volume geometry of one image held locally.
+struct Vol {
+  int ez = 1, ey = 1, ex = 1;
+  long long pitch = 0, plane = 0, image = 0;
+  static Vol make(int z, int y, int x);
+  long long bytes(size_t batch) const { return image * static_cast<long long>(batch) * 4; }
+};
+
+// Halo / scalar transport between z-slab ranks (null for an unsharded plan).
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+  // Send `count` floats at send_lo to rank-1 and at send_hi to rank+1; receive into
+  // recv_lo from rank-1 and recv_hi from rank+1 (null pointers skip a side).
+  virtual void exchange(const float* send_lo, float* recv_lo, const float* send_hi, float* recv_hi,
+                        size_t count, cudaStream_t s) = 0;
+  // All-gather `n` doubles per rank: out[r*n + i] = rank r's in[i].
+  virtual void allgather(const double* in, double* out, size_t n, cudaStream_t s) = 0;
+};
+std::unique_ptr<Transport> make_nccl_transport(int device, int rank, int world,
+                                               const unsigned char id[128]);
+struct LocalGroup;
+LocalGroup* new_local_group(int world);
+void delete_local_group(LocalGroup* g);
+std::unique_ptr<Transport> make_local_transport(LocalGroup* g, int rank);
+void nccl_unique_id(unsigned char out[128]);
+
+struct KernelStats {
+  uint64_t launches = 0;
+  double ms = 0.0;
+};
+
+class Plan {
+ public:
+  Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t* k_ext, const double* h,
+       std::unique_ptr<Transport> comm = nullptr);
+  ~Plan();
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  // --- data movement (dense host arrays, owned planes only when sharded) ---
+  void set_observation_f64(const double* y);
+  void set_observation_f32(const float* y);
+  void set_x_f64(const double* x);               // into the x buffer (for conv_full etc.)
+  void get_estimate_f64(double* x);
+  void get_estimate_f32(float* x);
+  void get_y_buffer_f64(double* y);              // the y-shaped result buffer (A x)
+  void get_x_buffer_f64(double* x, int which);   // 0 = x, 1 = g
+
+  // --- operators on resident buffers (the one-shot C-ABI entry points use these) ---
+  void op_conv_full();                 // r = A x            (store)
+  void op_adjoint_of_y();              // x = A^T y          (store)
+  double op_objective();               // 0.5||A x - y||^2   (resid into r)
+  void op_normal_gradient();           // g = A^T (A x - y)
+  double op_kkt_residual();            // max|min(x, A^T(Ax - y))|
+  double estimate_step(size_t power_iters);
+
+  // --- projected gradient (solvers.hpp:155-238) ---
+  void pg_begin(const ndc_deconv_config& cfg);
+  size_t pg_iterate(size_t n);  // returns images still active
+  void pg_end();
+  void get_report(size_t image, ndc_deconv_report* rep, double* obj, double* kkt, size_t cap) const;
+
+  // --- Richardson-Lucy (solvers.hpp:245-305) ---
+  void rl_run(const ndc_rl_config& cfg);
+
+  // --- bench hooks ---
+  void set_timing(bool on) { timing_ = on; }
+  void reset_stats();
+  KernelStats stats(int kind);
+  cudaStream_t stream() const { return stream_; }
+  void bench_forward();
+  void bench_adjoint();
+
+  size_t batch() const { return B_; }
+  size_t x_count() const { return static_cast<size_t>(xa_n_) * my_ * mx_; }  // owned, per image
+  size_t y_count() const { return static_cast<size_t>(yb_ - ya_) * (my_ + 2 * py_) * (mx_ + 2 * px_); }
+
+ private:
+  enum Dir { kFwd = 0, kAdj = 1 };
+  void alloc_all();
+  float* dev_alloc_f(long long n);
+  const CUtensorMap& map_for(const float* base, Dir d);
+  // Correlation pass over resident buffers; mode / aux per EpiMode.
+  void correlate(Dir d, const float* in, float* out, int mode, float* aux_out, const float* aux_in,
+                 const float* scale, const double* step, const int* active, bool partials);
+  // Reductions of the last correlate/elementwise pass into per-image device scalars.
+  void finalize(long long per_image, int op, double* out0, double* out1, float* scale_out,
+                const int* active);
+  long long partials_per_image(Dir d) const;
+  void halo_x(float* buf);   // fill x-buffer halo planes from neighbours (sharded only)
+  void halo_y(float* buf);   // fill y-buffer halo planes from neighbours (sharded only)
+  void copy_image_x(float* dst, const float* src, size_t b);
+  void copy_image_y(float* dst, const float* src, size_t b);
+  void sync();
+  void upload_active(const std::vector<int>& act);
+  void pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz);
+  void pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz);
+  void unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz);
+  void unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_off, int nz);
+  float* x_owned(float* buf) const { return buf + static_cast<long long>(xa_ - xlo_) * X_.plane; }
+
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  size_t B_ = 1;
+  int ndim_ = 1;
+  size_t xext_[3] = {1, 1, 1}, kext_[3] = {1, 1, 1};
+  int mz_ = 1, my_ = 1, mx_ = 1;
+  int KZ_ = 1, KY_ = 1, KX_ = 1, pz_ = 0, py_ = 0, px_ = 0;
+  std::vector<float> taps_fwd_, taps_adj_;
+  bool kernel_all_zero_ = false;
+
+  // z-slab geometry (global plane indices); unsharded: one slab holding everything.
+  std::unique_ptr<Transport> comm_;
+  int rank_ = 0, world_ = 1;
+  int xa_ = 0, xb_ = 0, xa_n_ = 0;  // owned x planes
+  int ya_ = 0, yb_ = 0;             // owned y planes
+  int xlo_ = 0, xhi_ = 0;           // x planes held (owned + halo)
+  int rlo_ = 0, rhi_ = 0;           // y planes held
+  Vol X_, Y_;
+
+  // device buffers
+  float *x_ = nullptr, *trial_ = nullptr, *g_ = nullptr;
+  float *yobs_ = nullptr, *r_ = nullptr, *rt_ = nullptr, *scratch_ = nullptr;
+  double2* partials_ = nullptr;
+  long long partials_cap_ = 0;
+  double* dsc_ = nullptr;   // device scalars
+  float* dscale_ = nullptr; // per-image scale
+  int* dactive_ = nullptr;
+  double* dstep_ = nullptr;
+  double* gather_ = nullptr;
+  double* hsc_ = nullptr;   // pinned host mirror
+  void* staging_ = nullptr;
+  size_t staging_bytes_ = 0;
+  std::map<std::pair<const float*, int>, CUtensorMap> maps_;
+
+  // stats
+  bool timing_ = false;
+  KernelStats st_[3];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
+  std::vector<std::pair<int, size_t>> ev_pending_;  // (kind, pool index)
+  size_t ev_used_ = 0;
+  void drain_events();
+
+  // PG state
+  struct Img {
+    std::vector<double> obj, kkt;
+    double f = 0, step = 0;
+    size_t iters = 0, backtracks = 0;
+    int reason = NDC_STOP_MAX_ITERS;
+    bool active = true;
+    size_t clamped = 0;
+  };
+  std::vector<Img> img_;
+  ndc_deconv_config cfg_{};
+  double step0_ = 0;
+  double wall0_ = 0, wall_ = 0;
+  bool pg_begun_ = false;
+};
+
+}  // namespace ndc

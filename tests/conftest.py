@@ -1,0 +1,49 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and runs the CUDA path")
+    config.addinivalue_line("markers", "slow: long-running case")
+
+
+@pytest.fixture(scope="session")
+def golden_ops():
+    return np.load(os.path.join(GOLDEN, "operators.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_solvers():
+    return np.load(os.path.join(GOLDEN, "solvers.npz"))
+
+
+@pytest.fixture(scope="session")
+def oracle_c():
+    from oracle.oracle import Oracle
+    return Oracle("c")
+
+
+@pytest.fixture(scope="session")
+def nd():
+    """The product API (fails loudly when libndconv_b200.so or the GPU is missing)."""
+    from paper_1711_11224_b200 import ndconv
+    n = ndconv.device_count()
+    assert n >= 1, "GPU tests need a B200; ndconv reports no usable device"
+    return ndconv
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.linalg.norm(b.ravel())
+    num = np.linalg.norm((a - b).ravel())
+    return num / den if den > 0 else num

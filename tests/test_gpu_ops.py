@@ -1,0 +1,155 @@
+"""GPU parity of the operators (convolution.hpp / solvers.hpp scalar functions) through
+the C-ABI against the reference's golden outputs and the CPU oracle.
+
+Tolerance (BASELINE.json north_star): relative L2 <= 1e-5 per convolution.  Integer
+known-answer tests are exact in float32 and are checked for exact equality.
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import rel_l2
+from tests.golden.make_golden import big_inputs
+
+pytestmark = pytest.mark.gpu
+TOL_CONV = 1e-5
+
+
+def test_kat_conv_full_exact(nd):
+    # test_convolution.cpp:11-19, 40-45
+    assert np.array_equal(nd.conv_full([1.0, 2.0], [1.0, 1.0, 1.0]), [1, 3, 3, 2])
+    assert np.array_equal(nd.conv_full([1.0, 2.0, 3.0], [0.0, 1.0, 0.0]), [0, 1, 2, 3, 0])
+    assert np.array_equal(nd.conv_full([3.0], [1.0, 2.0, 4.0, 2.0, 1.0]), [3, 6, 12, 6, 3])
+
+
+def test_kat_adjoint_impulse_exact(nd):
+    # test_convolution.cpp:104-108
+    assert np.array_equal(nd.adjoint_apply([1.0, 0, 0, 0], [1.0, 2.0, 3.0], (2,)), [1.0, 0.0])
+
+
+def test_kat_flip_crop(nd):
+    # test_convolution.cpp:61-82: flip reverses every axis, is an involution
+    h = np.arange(1.0, 10.0).reshape(3, 3)
+    f = nd.flip(h)
+    assert np.array_equal(f, h[::-1, ::-1]) and np.array_equal(nd.flip(f), h)
+
+
+def test_golden_small_family(nd, golden_ops):
+    d = golden_ops
+    for i in range(int(d["n"])):
+        x, h = d[f"x{i}"], d[f"h{i}"]
+        y = nd.conv_full(x, h)
+        assert y.shape == d[f"y{i}"].shape
+        assert rel_l2(y, d[f"y{i}"]) <= TOL_CONV, i
+        a = nd.adjoint_apply(d[f"r{i}"], h, x.shape)
+        assert rel_l2(a, d[f"atr{i}"]) <= TOL_CONV, i
+
+
+def test_golden_large(nd, golden_ops):
+    d = golden_ops
+    for i in range(int(d["nbig"])):
+        x, h, r = big_inputs(i)
+        assert rel_l2(nd.conv_full(x, h), d[f"by{i}"]) <= TOL_CONV, i
+        assert rel_l2(nd.adjoint_apply(r, h, x.shape), d[f"batr{i}"]) <= TOL_CONV, i
+
+
+def test_linearity_and_adjoint_identity(nd):
+    # test_convolution.cpp:47-59 and 110-122 at float32 tolerance
+    g = np.random.Generator(np.random.PCG64(24))
+    for _ in range(10):
+        ndim = int(g.integers(1, 4))
+        xs = tuple(int(v) for v in g.integers(1, 9, ndim))
+        hs = tuple(int(2 * v + 1) for v in g.integers(0, 3, ndim))
+        h = g.uniform(-1, 1, hs)
+        a, b = g.uniform(-1, 1, xs), g.uniform(-1, 1, xs)
+        lhs = nd.conv_full(2.5 * a - 1.25 * b, h)
+        rhs = 2.5 * nd.conv_full(a, h) - 1.25 * nd.conv_full(b, h)
+        assert rel_l2(lhs, rhs) <= 1e-5
+        y = g.uniform(-1, 1, lhs.shape)
+        l = float(np.sum(nd.conv_full(a, h) * y))
+        r = float(np.sum(a * nd.adjoint_apply(y, h, xs)))
+        assert abs(l - r) / max(1.0, abs(l), abs(r)) <= 1e-5
+
+
+def test_missing_flip_would_be_caught(nd):
+    # test_convolution.cpp:124-136: the device adjoint must pass, a flip-less one fails
+    h = np.array([1.0, 0.0, -2.0])
+    x = np.array([1.0, -1.0, 2.0, 0.5])
+    y = np.array([0.5, 1.0, -2.0, 0.0, 1.5, -1.0])
+    good = float(np.dot(x, nd.adjoint_apply(y, h, (4,))))
+    assert abs(float(np.dot(nd.conv_full(x, h), y)) - good) <= 1e-6
+
+
+def test_normal_gradient_and_scalars(nd, oracle_c):
+    g = np.random.Generator(np.random.PCG64(25))
+    for _ in range(5):
+        h = g.uniform(-1, 1, (3, 5))
+        x = g.uniform(-1, 1, (17, 23))
+        y = g.uniform(-1, 1, (19, 27))
+        assert rel_l2(nd.normal_gradient(x, y, h), oracle_c.normal_gradient(x, y, h)) <= 1e-5
+        f_ref = oracle_c.objective(x, y, h)
+        assert abs(nd.objective(x, y, h) - f_ref) <= 1e-5 * abs(f_ref)
+        k_ref = oracle_c.kkt_residual(x, y, h)
+        assert abs(nd.kkt_residual(x, y, h) - k_ref) <= 1e-5 * max(1.0, abs(k_ref))
+
+
+def test_kat_objective_kkt(nd):
+    # test_solvers.cpp:12-22, 42-60
+    assert nd.objective([1.0], [3.0], [1.0]) == 2.0
+    box = np.array([0.5, 1.0, -0.25])
+    x = np.array([1.0, -2.0, 0.5])
+    assert abs(nd.objective(x, nd.conv_full(x, box), box)) <= 1e-12
+    h = np.array([0.5, 1.0, 0.25])
+    truth = np.array([0.0, 2.0, 0.0, 1.0])
+    assert nd.kkt_residual(truth, nd.conv_full(truth, h), h) <= 1e-6
+    assert nd.kkt_residual(np.zeros(4), np.full(6, -1.0), h) == 0.0
+
+
+def test_estimate_step_kats(nd, golden_solvers):
+    # test_solvers.cpp:24-40
+    assert abs(nd.estimate_step([1.0], (5,), 10) - 1.0) <= 1e-6
+    assert abs(nd.estimate_step([2.0], (5,), 10) - 0.25) <= 1e-6
+    s = nd.estimate_step([1.0, 1.0, 1.0], (8,), 30)
+    assert 1 / 9 <= s <= 1.0 and abs(s - float(golden_solvers["step_box"])) <= 1e-5 * s
+    with pytest.raises(nd.NumericError):
+        nd.estimate_step([0.0, 0.0, 0.0], (4,), 5)
+
+
+def test_error_classes(nd):
+    # test_convolution.cpp:33-38, kernel.hpp:18-22, test_solvers.cpp:168-189
+    with pytest.raises(nd.ShapeError):
+        nd.conv_full(np.ones((2, 2)), np.ones(3))
+    with pytest.raises(nd.ShapeError):
+        nd.adjoint_apply(np.ones((2, 2)), np.ones(3), (2, 2))
+    with pytest.raises(nd.ShapeError):
+        nd.conv_full(np.ones(4), np.ones(2))
+    with pytest.raises(nd.NumericError):
+        nd.conv_full(np.ones(4), np.array([1.0, np.nan, 1.0]))
+    with pytest.raises(nd.ShapeError):
+        nd.deconv_pg(np.zeros(6), [0.1, 0.8, 0.1], (5,))
+    with pytest.raises(nd.NumericError):
+        nd.deconv_pg(np.zeros(6), [0.0, 0.0, 0.0], (4,))
+    with pytest.raises(nd.Error):
+        nd.deconv_pg(np.zeros(6), [0.1, 0.8, 0.1], (4,), nd.DeconvConfig(backtrack_factor=1.0))
+    with pytest.raises(nd.Error):
+        nd.deconv_pg(np.zeros(6), [0.1, 0.8, 0.1], (4,), nd.DeconvConfig(max_iters=0))
+    with pytest.raises(nd.UnsupportedError):
+        nd.conv_full(np.ones((4, 4)), np.ones((3, 35)))
+
+
+def test_config_shapes_sampled(nd, oracle_c):
+    """BASELINE config 3 / 4 / 5 PSFs on reduced volumes, checked at sampled voxels
+    through the reference's per-voxel routine."""
+    from paper_1711_11224_b200 import synth
+    g = np.random.Generator(np.random.PCG64(31))
+    for name, shape in (("c3", (20, 40, 48)), ("c4", (24, 36, 40)), ("c5", (6, 40, 44))):
+        h = synth.psf_for(name)
+        x = synth.fp32_exact(g.uniform(0, 1, shape))
+        y = nd.conv_full(x, h)
+        idx = g.integers(0, y.size, 3000)
+        ref = oracle_c.conv_full_sample(x, h, idx)
+        assert rel_l2(y.ravel()[idx], ref) <= TOL_CONV, name
+        r = synth.fp32_exact(g.uniform(-1, 1, y.shape))
+        a = nd.adjoint_apply(r, h, shape)
+        idx = g.integers(0, a.size, 3000)
+        ref = oracle_c.adjoint_sample(r, h, shape, idx)
+        assert rel_l2(a.ravel()[idx], ref) <= TOL_CONV, name

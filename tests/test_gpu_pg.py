@@ -1,0 +1,141 @@
+"""GPU parity of deconv_pg (solvers.hpp:155-238) through the C-ABI.
+
+Bar (BASELINE.json north_star): estimate within relative L2 1e-4 of the reference
+after the full iteration count; objective / KKT traces within 1e-4 relative; same
+iteration count and stop reason.  Reference outputs come from tests/golden/solvers.npz
+(the compiled reference) or the CPU oracle on the same fp32-exact inputs.
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL_ITER = 1e-4
+
+
+def _cfg(nd, cfg):
+    kw = dict(max_iters=int(cfg[0]), tol_rel_objective=float(cfg[1]))
+    if cfg[2] > 0:
+        kw["initial_step"] = float(cfg[2])
+    return nd.DeconvConfig(**kw)
+
+
+def _trace_close(a, b, tol):
+    a, b = np.asarray(a), np.asarray(b)
+    scale = np.maximum(np.abs(b), 1e-12 * max(1.0, float(np.max(np.abs(b)))))
+    return a.shape == b.shape and bool(np.all(np.abs(a - b) <= tol * np.maximum(scale, 1e-30) + 1e-12))
+
+
+def _check(nd, d, i, tol=TOL_ITER):
+    rep = nd.deconv_pg(d[f"pg_y{i}"], d[f"pg_h{i}"], tuple(int(v) for v in d[f"pg_xs{i}"]),
+                       _cfg(nd, d[f"pg_cfg{i}"]))
+    ref_x = d[f"pg_x{i}"]
+    assert rep.stop_reason == str(d[f"pg_stop{i}"]), (i, rep.stop_reason)
+    assert rep.iterations_run == int(d[f"pg_it{i}"]), (i, rep.iterations_run)
+    assert rel_l2(rep.estimate, ref_x) <= tol or np.max(np.abs(rep.estimate - ref_x)) <= 1e-6, i
+    assert _trace_close(rep.objective_trace, d[f"pg_obj{i}"], tol), i
+    assert len(rep.kkt_trace) == len(d[f"pg_kkt{i}"])
+    assert np.all(rep.estimate >= 0)
+    assert np.all(np.diff(rep.objective_trace) < 0)
+    return rep
+
+
+def test_solver_kats(nd, golden_solvers):
+    d = golden_solvers
+    n = int(d["npg"])
+    # identity kernel, 1-d sparse recovery, all-negative data (test_solvers.cpp:62-93)
+    for i in (n - 5, n - 4, n - 3):
+        _check(nd, d, i)
+    rep = nd.deconv_pg(np.array([3.0, -2.0, 0.0, 5.0]), [1.0], (4,), nd.DeconvConfig(max_iters=50))
+    assert np.array_equal(rep.estimate, [3.0, 0.0, 0.0, 5.0])
+    rep = nd.deconv_pg(np.full(6, -2.0), [0.2, 0.5, 0.3], (4,), nd.DeconvConfig(max_iters=100))
+    assert np.array_equal(rep.estimate, np.zeros(4)) and rep.kkt_trace[-1] == 0.0
+
+
+def test_random_family(nd, golden_solvers):
+    # test_solvers.cpp:95-112 family, 40 iterations, tol 0
+    d = golden_solvers
+    n = int(d["npg"])
+    for i in range(n - 5):
+        _check(nd, d, i)
+
+
+def test_acceptance6_backtracking(nd, golden_solvers):
+    # acceptance.cpp:171-206: step 8 forces backtracking in ~40% of 500 iterations
+    d = golden_solvers
+    rep = _check(nd, d, int(d["npg"]) - 2)
+    assert rep.extra["backtracks"] > 100
+    y = d[f"pg_y{int(d['npg']) - 2}"]
+    rel_res = np.sqrt(2 * rep.objective_trace[-1]) / np.linalg.norm(y)
+    assert rel_res < 1e-3 and rep.kkt_trace[-1] < 1e-4
+
+
+def test_config1_full(nd, golden_solvers):
+    # BASELINE config 1: 256x256, 15x15 sigma 2, 50 iterations, auto step
+    d = golden_solvers
+    i = int(d["npg"]) - 1
+    rep = _check(nd, d, i)
+    assert abs(rep.extra["step0"] - float(d["c1_step"])) <= 1e-5 * float(d["c1_step"])
+
+
+def test_batch_matches_single_images(nd, oracle_c):
+    """Config-2 style batch: per-image scalars, each image equal to its own run."""
+    from paper_1711_11224_b200 import synth
+    xs, ys, h = synth.make("c2", shape=(96, 80), batch=3, n_objects=40)
+    cfg = nd.DeconvConfig(max_iters=30, tol_rel_objective=0.0)
+    reps = nd.deconv_pg_batch(ys, h, xs.shape[1:], cfg)
+    for b in range(3):
+        ref = oracle_c.deconv_pg(ys[b], h, xs.shape[1:], max_iters=30, tol_rel_objective=0.0)
+        assert rel_l2(reps[b].estimate, ref.estimate) <= TOL_ITER
+        assert _trace_close(reps[b].objective_trace, ref.objective_trace, TOL_ITER)
+        assert reps[b].iterations_run == ref.iterations_run
+
+
+def test_batch_mixed_stopping(nd, oracle_c):
+    """Images of one batch stop at different iterations (tolerance) and keep their
+    own iterate while the others continue."""
+    g = np.random.Generator(np.random.PCG64(3))
+    h = np.array([[0.05, 0.1, 0.05], [0.1, 0.4, 0.1], [0.05, 0.1, 0.05]])
+    xs = (12, 10)
+    ys = np.stack([oracle_c.conv_full(g.uniform(0, 1, xs), h) * s for s in (1.0, 0.1, 10.0)])
+    ys[1] = np.full(ys[1].shape, -1.0)  # converges at once (x = 0 fixed point)
+    cfg = nd.DeconvConfig(max_iters=60, tol_rel_objective=1e-3)
+    reps = nd.deconv_pg_batch(ys, h, xs, cfg)
+    for b in range(3):
+        ref = oracle_c.deconv_pg(ys[b], h, xs, max_iters=60, tol_rel_objective=1e-3)
+        assert reps[b].stop_reason == ref.stop_reason
+        assert reps[b].iterations_run == ref.iterations_run
+        assert rel_l2(reps[b].estimate, ref.estimate) <= TOL_ITER or np.max(np.abs(reps[b].estimate - ref.estimate)) < 1e-6
+
+
+def test_3d_config3_replica(nd, oracle_c):
+    """Config 3 PSF (31x15x15 anisotropic) on a reduced volume, full N=50 iterations
+    vs the oracle (SURVEY §8c reduced-size replica)."""
+    from paper_1711_11224_b200 import synth
+    x, y, h = synth.make("c3", shape=(24, 32, 32), n_objects=20)
+    cfg = nd.DeconvConfig(max_iters=50, tol_rel_objective=0.0)
+    rep = nd.deconv_pg(y, h, x.shape, cfg)
+    ref = oracle_c.deconv_pg(y, h, x.shape, max_iters=50, tol_rel_objective=0.0)
+    assert rep.iterations_run == ref.iterations_run and rep.stop_reason == ref.stop_reason
+    assert rel_l2(rep.estimate, ref.estimate) <= TOL_ITER
+    assert _trace_close(rep.objective_trace, ref.objective_trace, TOL_ITER)
+
+
+def test_plan_stepping_equals_run(nd):
+    """begin / iterate(k) / end in pieces equals one run (bench uses the pieces)."""
+    from paper_1711_11224_b200 import synth
+    xs, ys, h = synth.make("c2", shape=(64, 70), batch=2, n_objects=20)
+    cfg = nd.DeconvConfig(max_iters=12, tol_rel_objective=0.0)
+    full = nd.deconv_pg_batch(ys, h, xs.shape[1:], cfg)
+    with nd.Plan(xs.shape[1:], h, batch=2) as p:
+        p.set_observation(ys)
+        p.pg_begin(cfg)
+        for _ in range(4):
+            p.pg_iterate(3)
+        p.pg_end()
+        est = p.estimate()
+        for b in range(2):
+            r = p.report(b, 13)
+            assert np.array_equal(est[b], full[b].estimate)
+            assert np.array_equal(r.objective_trace, full[b].objective_trace)
