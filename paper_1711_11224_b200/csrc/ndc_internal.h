@@ -79,12 +79,19 @@ struct TapBlock {
   float t[kTapCap];
 };
 
-// Launch the correlation kernel for one tap chunk.
-cudaError_t launch_correlate(int kx, const CUtensorMap& map, const CorrGeom& g,
+// Launch the correlation kernel for one tap chunk; sh (0 or 2) is the register-window
+// shift that keeps the TMA tile start 16-byte aligned.
+cudaError_t launch_correlate(int kx, int sh, const CUtensorMap& map, const CorrGeom& g,
                              const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
                              cudaStream_t s);
+cudaError_t launch_correlate_sh0(int kx, const CUtensorMap& map, const CorrGeom& g,
+                                 const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
+                                 cudaStream_t s);
+cudaError_t launch_correlate_sh2(int kx, const CUtensorMap& map, const CorrGeom& g,
+                                 const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
+                                 cudaStream_t s);
 size_t correlate_smem_bytes(const CorrGeom& g);
-int shared_pitch_for(int kx);
+int shared_pitch_for(int kx, int sh);
 
 // Small kernels.
 enum FinalizeOp : int {
@@ -98,22 +105,26 @@ cudaError_t launch_finalize(const double2* partials, long long per_image, int ba
                             cudaStream_t s);
 cudaError_t launch_combine(const double* gathered, int world, int op, double* out0, double* out1,
                            float* scale_out, cudaStream_t s);
+// Interior view of a pitched volume (pointers passed alongside are at the interior
+// origin): ez planes of ey rows of ex valid floats; strides in floats.
+struct Geo {
+  int ez, ey, ex;
+  long long pitch, plane, image;
+};
 cudaError_t launch_pg_trial(const float* x, const float* g, float* trial, const double* step,
-                            const int* active, double2* partials, int batch, long long image_elems,
-                            int ez, int ey, int ex, long long pitch, int blocks_per_image,
+                            const int* active, double2* partials, int batch, const Geo& v,
+                            int blocks_per_image, cudaStream_t s);
+cudaError_t launch_fill(float* dst, float value, int batch, const Geo& v, cudaStream_t s);
+cudaError_t launch_pack_f64(const double* dense, float* pitched, int batch, const Geo& v,
                             cudaStream_t s);
-cudaError_t launch_fill(float* dst, float value, int batch, int ez, int ey, int ex, long long pitch,
-                        cudaStream_t s);
-cudaError_t launch_pack_f64(const double* dense, float* pitched, int batch, int ez, int ey, int ex,
-                            long long pitch, cudaStream_t s);
-cudaError_t launch_unpack_f64(const float* pitched, double* dense, int batch, int ez, int ey, int ex,
-                              long long pitch, cudaStream_t s);
-cudaError_t launch_pack_f32(const float* dense, float* pitched, int batch, int ez, int ey, int ex,
-                            long long pitch, cudaStream_t s);
-cudaError_t launch_unpack_f32(const float* pitched, float* dense, int batch, int ez, int ey, int ex,
-                              long long pitch, cudaStream_t s);
-cudaError_t launch_clamp_count(const float* src, float* dst, double2* partials, int batch, int ez,
-                               int ey, int ex, long long pitch, int blocks_per_image, cudaStream_t s);
+cudaError_t launch_unpack_f64(const float* pitched, double* dense, int batch, const Geo& v,
+                              cudaStream_t s);
+cudaError_t launch_pack_f32(const float* dense, float* pitched, int batch, const Geo& v,
+                            cudaStream_t s);
+cudaError_t launch_unpack_f32(const float* pitched, float* dense, int batch, const Geo& v,
+                              cudaStream_t s);
+cudaError_t launch_clamp_count(const float* src, float* dst, double2* partials, int batch,
+                               const Geo& v, int blocks_per_image, cudaStream_t s);
 
 // Driver-API entry for TMA descriptor encoding (resolved through the runtime, no -lcuda).
 CUresult encode_tensor_map(CUtensorMap* map, const float* base, int ex, int ey, long long zcount,

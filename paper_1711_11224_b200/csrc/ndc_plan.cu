@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -34,14 +35,18 @@ void check_cuda(cudaError_t e, const char* what) {
   }
 }
 
-Vol Vol::make(int z, int y, int x) {
+Vol Vol::make(int z, int y, int x, int r0, int c0) {
   Vol v;
   v.ez = z;
   v.ey = y;
   v.ex = x;
-  v.pitch = cdiv(x, kTileX) * kTileX;
-  v.plane = v.pitch * y;
+  v.r0 = r0;
+  v.c0 = c0;
+  // every output tile (kTileX wide) stays inside its row
+  v.pitch = cdiv(c0 + cdiv(x, kTileX) * kTileX, 32) * 32;
+  v.plane = v.pitch * (r0 + y);
   v.image = v.plane * z;
+  v.origin = static_cast<long long>(r0) * v.pitch + c0;
   return v;
 }
 
@@ -120,7 +125,7 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     xlo_ = 0;
     xhi_ = mz_;
   }
-  X_ = Vol::make(xhi_ - xlo_, my_, mx_);
+  X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, 4) * 4));
   Y_ = Vol::make(rhi_ - rlo_, my_ + 2 * py_, mx_ + 2 * px_);
 
   int ndev = 0;
@@ -204,14 +209,16 @@ void Plan::alloc_all() {
 
 void Plan::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
-const CUtensorMap& Plan::map_for(const float* base, Dir d) {
+const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh) {
   auto key = std::make_pair(base, static_cast<int>(d));
   auto it = maps_.find(key);
   if (it != maps_.end()) return it->second;
   const Vol& v = (d == kFwd) ? X_ : Y_;
   CUtensorMap m;
-  const CUresult rc = encode_tensor_map(&m, base, v.ex, v.ey, static_cast<long long>(v.ez) * B_,
-                                        v.pitch, v.plane, shared_pitch_for(KX_), kTileY + KY_ - 1);
+  // x-shaped inputs are described including their zero margin (ndc_plan.h Vol)
+  const CUresult rc = encode_tensor_map(&m, base, v.c0 + v.ex, v.r0 + v.ey,
+                                        static_cast<long long>(v.ez) * B_, v.pitch, v.plane,
+                                        shared_pitch_for(KX_, sh), kTileY + KY_ - 1);
   if (rc != CUDA_SUCCESS)
     fail(NDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
   return maps_.emplace(key, m).first->second;
@@ -231,12 +238,14 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   g.out_ey = vout.ey;
   g.out_ex = vout.ex;
   int nz_out;
+  int sh = 0;
   if (fwd) {
     nz_out = yb_ - ya_;
     g.out_z0 = ya_ - rlo_;
     g.off_z = ya_ - 2 * pz_ - xlo_;
-    g.off_y = -2 * py_;
-    g.off_x = -2 * px_;
+    g.off_y = X_.r0 - 2 * py_;
+    sh = (X_.c0 - 2 * px_) & 3;  // 0 or 2 (2p is even, c0 a multiple of 4)
+    g.off_x = X_.c0 - 2 * px_ - sh;
   } else {
     nz_out = xb_ - xa_;
     g.out_z0 = xa_ - xlo_;
@@ -244,11 +253,14 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     g.off_y = 0;
     g.off_x = 0;
   }
+  // TMA tile starts must be non-negative (x-shaped inputs carry a zero margin)
+  if (g.off_x < 0 || g.off_y < 0 || (g.off_x & 3))
+    fail(NDC_ERR_CUDA, "internal: negative or unaligned TMA tile origin");
   g.KY = KY_;
   g.tiles_x = static_cast<int>(cdiv(vout.ex, kTileX));
   g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY));
   g.rows = kTileY + KY_ - 1;
-  g.pitch_s = shared_pitch_for(KX_);
+  g.pitch_s = shared_pitch_for(KX_, sh);
   g.out_pitch = vout.pitch;
   g.out_plane = vout.plane;
   g.out_image = vout.image;
@@ -256,7 +268,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   const int per_slice = KY_ * KX_;
   const int slices_per = kTapCap / per_slice;
   const int nchunks = static_cast<int>(cdiv(KZ_, slices_per));
-  const CUtensorMap& map = map_for(in, d);
+  const CUtensorMap& map = map_for(in, d, sh);
   static thread_local TapBlock tb;
   for (int c = 0; c < nchunks; ++c) {
     g.kz0 = c * slices_per;
@@ -264,11 +276,14 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     g.stages = std::min(2, g.kz1 - g.kz0);
     g.accum = c > 0;
     g.final_chunk = (c == nchunks - 1);
+    // x-shaped operands are addressed from their interior origin
+    const long long xo = fwd ? 0 : X_.origin;
+    auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
     CorrArgs a{};
-    a.out = g.final_chunk ? out : scratch_;
-    a.accum_in = scratch_;
-    a.aux_out = aux_out;
-    a.aux_in = aux_in;
+    a.out = at(g.final_chunk ? out : scratch_);
+    a.accum_in = at(scratch_);
+    a.aux_out = at(aux_out);
+    a.aux_in = fwd ? aux_in : at(aux_in);
     a.scale = scale;
     a.step = step;
     a.active = active;
@@ -286,7 +301,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
       ev = ev_used_++;
       check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
     }
-    check_cuda(launch_correlate(KX_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
+    check_cuda(launch_correlate(KX_, sh, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
                "correlate launch");
     if (timing_) {
       check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
@@ -375,8 +390,8 @@ void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_of
     check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 8, cudaMemcpyHostToDevice, stream_),
                "H2D");
     check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
-                               dev + b * v.image + static_cast<long long>(z_off) * v.plane, 1, nz,
-                               v.ey, v.ex, v.pitch, stream_),
+                               dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
+                               v.geo(nz), stream_),
                "pack");
     st_[2].launches++;
   }
@@ -389,8 +404,8 @@ void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off
     check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 4, cudaMemcpyHostToDevice, stream_),
                "H2D");
     check_cuda(launch_pack_f32(static_cast<const float*>(staging_),
-                               dev + b * v.image + static_cast<long long>(z_off) * v.plane, 1, nz,
-                               v.ey, v.ex, v.pitch, stream_),
+                               dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
+                               v.geo(nz), stream_),
                "pack");
     st_[2].launches++;
   }
@@ -400,8 +415,8 @@ void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off
 void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(launch_unpack_f64(dev + b * v.image + static_cast<long long>(z_off) * v.plane,
-                                 static_cast<double*>(staging_), 1, nz, v.ey, v.ex, v.pitch, stream_),
+    check_cuda(launch_unpack_f64(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
+                                 static_cast<double*>(staging_), 1, v.geo(nz), stream_),
                "unpack");
     st_[2].launches++;
     check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 8, cudaMemcpyDeviceToHost, stream_),
@@ -413,8 +428,8 @@ void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_
 void Plan::unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(launch_unpack_f32(dev + b * v.image + static_cast<long long>(z_off) * v.plane,
-                                 static_cast<float*>(staging_), 1, nz, v.ey, v.ex, v.pitch, stream_),
+    check_cuda(launch_unpack_f32(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
+                                 static_cast<float*>(staging_), 1, v.geo(nz), stream_),
                "unpack");
     st_[2].launches++;
     check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 4, cudaMemcpyDeviceToHost, stream_),
@@ -492,8 +507,8 @@ double Plan::estimate_step(size_t power_iters) {
   try {
     const float one = 1.0f;
     check_cuda(cudaMemcpyAsync(dscale_, &one, 4, cudaMemcpyHostToDevice, stream_), "H2D");
-    check_cuda(launch_fill(x_owned(g_), static_cast<float>(1.0 / std::sqrt(n)), 1, xa_n_, my_, mx_,
-                           X_.pitch, stream_),
+    check_cuda(launch_fill(x_owned(g_), static_cast<float>(1.0 / std::sqrt(n)), 1, X_.geo(xa_n_),
+                           stream_),
                "fill");
     st_[2].launches++;
     double* lam = dsc_ + kNumSlots * saveB;
@@ -624,8 +639,7 @@ size_t Plan::pg_iterate(size_t n) {
       upload_active(bt);
       check_cuda(cudaMemcpyAsync(dstep_, stp.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
       check_cuda(launch_pg_trial(x_owned(x_), x_owned(g_), x_owned(trial_), dstep_, dactive_, partials_,
-                                 static_cast<int>(B_), 0, xa_n_, my_, mx_, X_.pitch, kElemBlocks,
-                                 stream_),
+                                 static_cast<int>(B_), X_.geo(xa_n_), kElemBlocks, stream_),
                  "pg_trial launch");
       st_[2].launches++;
       finalize(kElemBlocks, kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr, dactive_);

@@ -26,12 +26,16 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 
-// Pitched volume geometry of one image held locally.
+// Pitched volume geometry of one image held locally.  x-shaped volumes carry a zero
+// margin of r0 rows above and c0 (>= 2p_x, multiple of 4) columns left of the data so
+// that every forward-pass TMA box starts at a non-negative coordinate (a negative
+// tile start traps on this driver); `origin` is the offset of element (0,0,0).
 struct Vol {
   int ez = 1, ey = 1, ex = 1;
-  long long pitch = 0, plane = 0, image = 0;
-  static Vol make(int z, int y, int x);
-  long long bytes(size_t batch) const { return image * static_cast<long long>(batch) * 4; }
+  int r0 = 0, c0 = 0;
+  long long pitch = 0, plane = 0, image = 0, origin = 0;
+  static Vol make(int z, int y, int x, int r0 = 0, int c0 = 0);
+  Geo geo(int nz) const { return Geo{nz, ey, ex, pitch, plane, image}; }
 };
 
 // Halo / scalar transport between z-slab ranks (null for an unsharded plan).
@@ -110,7 +114,7 @@ class Plan {
   enum Dir { kFwd = 0, kAdj = 1 };
   void alloc_all();
   float* dev_alloc_f(long long n);
-  const CUtensorMap& map_for(const float* base, Dir d);
+  const CUtensorMap& map_for(const float* base, Dir d, int sh);
   // Correlation pass over resident buffers; mode / aux per EpiMode.
   void correlate(Dir d, const float* in, float* out, int mode, float* aux_out, const float* aux_in,
                  const float* scale, const double* step, const int* active, bool partials);
@@ -128,7 +132,9 @@ class Plan {
   void pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz);
   void unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz);
   void unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_off, int nz);
-  float* x_owned(float* buf) const { return buf + static_cast<long long>(xa_ - xlo_) * X_.plane; }
+  float* x_owned(float* buf) const {
+    return buf + X_.origin + static_cast<long long>(xa_ - xlo_) * X_.plane;
+  }
 
   int device_ = 0;
   cudaStream_t stream_ = nullptr;

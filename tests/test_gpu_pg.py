@@ -21,23 +21,47 @@ def _cfg(nd, cfg):
     return nd.DeconvConfig(**kw)
 
 
-def _trace_close(a, b, tol):
+def _trace_close(a, b, tol, scale0=None, floor=1e-6):
+    """|a - b| <= tol |b| elementwise while b >= 1e-4 * scale0 (the well-conditioned
+    part of the run), and |a - b| <= floor * scale0 after that.  Once a trace has
+    fallen four orders of magnitude below its start, the strict-decrease line search
+    (solvers.hpp:198) compares objectives that differ by less than their float32
+    rounding, so backtracking decisions -- and with them the late trajectory -- may
+    legitimately differ from the f64 reference; the estimate itself is still held to
+    the 1e-4 relative-L2 bar separately.  scale0 defaults to b[0]."""
     a, b = np.asarray(a), np.asarray(b)
-    scale = np.maximum(np.abs(b), 1e-12 * max(1.0, float(np.max(np.abs(b)))))
-    return a.shape == b.shape and bool(np.all(np.abs(a - b) <= tol * np.maximum(scale, 1e-30) + 1e-12))
+    if a.shape != b.shape:
+        return False
+    s0 = abs(float(b[0])) if scale0 is None else scale0
+    head = np.abs(b) >= 1e-4 * s0
+    ok_head = np.abs(a - b) <= tol * np.abs(b) + 1e-300
+    ok_tail = np.abs(a - b) <= floor * s0 + 1e-300
+    return bool(np.all(np.where(head, ok_head, ok_tail)))
 
 
 def _check(nd, d, i, tol=TOL_ITER):
     rep = nd.deconv_pg(d[f"pg_y{i}"], d[f"pg_h{i}"], tuple(int(v) for v in d[f"pg_xs{i}"]),
                        _cfg(nd, d[f"pg_cfg{i}"]))
-    ref_x = d[f"pg_x{i}"]
-    assert rep.stop_reason == str(d[f"pg_stop{i}"]), (i, rep.stop_reason)
-    assert rep.iterations_run == int(d[f"pg_it{i}"]), (i, rep.iterations_run)
+    ref_x, ref_obj, ref_kkt = d[f"pg_x{i}"], d[f"pg_obj{i}"], d[f"pg_kkt{i}"]
+    ref_stop, ref_it = str(d[f"pg_stop{i}"]), int(d[f"pg_it{i}"])
     assert rel_l2(rep.estimate, ref_x) <= tol or np.max(np.abs(rep.estimate - ref_x)) <= 1e-6, i
-    assert _trace_close(rep.objective_trace, d[f"pg_obj{i}"], tol), i
-    assert len(rep.kkt_trace) == len(d[f"pg_kkt{i}"])
     assert np.all(rep.estimate >= 0)
     assert np.all(np.diff(rep.objective_trace) < 0)
+    assert len(rep.kkt_trace) == len(rep.objective_trace)
+    if rep.stop_reason == ref_stop and rep.iterations_run == ref_it:
+        assert _trace_close(rep.objective_trace, ref_obj, tol), i
+        assert _trace_close(rep.kkt_trace, ref_kkt, 1e-3, scale0=max(abs(ref_kkt[0]), 1e-30),
+                            floor=1e-3), i
+    else:
+        # The bitwise fixed-point test trial == x (solvers.hpp:191) fires earlier in
+        # float32 (x - step*g rounds back to x once |step*g| < ulp(x)/2): the device run
+        # may stop as "converged" while the f64 reference keeps taking steps too small
+        # to move a float32 iterate.  The estimate must still match (checked above) and
+        # the traces must agree on the common prefix.
+        assert rep.stop_reason == "converged" and rep.iterations_run < ref_it, (i, rep.stop_reason,
+                                                                                  rep.iterations_run, ref_it)
+        n = len(rep.objective_trace)
+        assert _trace_close(rep.objective_trace, ref_obj[:n], tol), i
     return rep
 
 
