@@ -18,8 +18,8 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libndconv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["ndc_corr_sh0.cu", "ndc_corr_sh2.cu", "ndc_kernels.cu", "ndc_plan.cu", "ndc_capi.cu",
-           "ndc_comm.cu"]
+SOURCES = ["ndc_corr_sh0_ry1.cu", "ndc_corr_sh0_ry2.cu", "ndc_corr_sh2_ry1.cu", "ndc_corr_sh2_ry2.cu",
+           "ndc_kernels.cu", "ndc_plan.cu", "ndc_capi.cu", "ndc_comm.cu"]
 HEADERS = ["ndc_internal.h", "ndc_plan.h", "ndc_correlate.cuh", os.path.join("..", "..", "include", "ndconv_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

@@ -50,6 +50,7 @@ enum EpiMode : int {
 // [0, in_ez) are skipped).
 struct CorrGeom {
   int in_ez, in_ey, in_ex;   // input buffer extents (planes held locally, rows, columns)
+  int in_row0;               // tensor row of input data row 0 (zero margin above it)
   int out_ey, out_ex;        // output rows / columns (valid region)
   int out_z0;                // buffer plane of computed output plane 0 (z-slab offset)
   int off_z, off_y, off_x;   // input coordinate = computed index + tap + off
@@ -79,17 +80,25 @@ struct TapBlock {
   float t[kTapCap];
 };
 
+// Tap rows are stored with an even pitch (64-bit aligned pairs in the parameter bank).
+__host__ __device__ constexpr int tap_pitch(int kx) { return (kx + 1) & ~1; }
+
 // Launch the correlation kernel for one tap chunk; sh (0 or 2) is the register-window
-// shift that keeps the TMA tile start 16-byte aligned.
-cudaError_t launch_correlate(int kx, int sh, const CUtensorMap& map, const CorrGeom& g,
+// shift that keeps the TMA tile start 16-byte aligned, ry (1 or 2) the output rows per
+// thread (tile height 64*ry).
+cudaError_t launch_correlate(int kx, int sh, int ry, const CUtensorMap& map, const CorrGeom& g,
                              const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
                              cudaStream_t s);
-cudaError_t launch_correlate_sh0(int kx, const CUtensorMap& map, const CorrGeom& g,
-                                 const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
-                                 cudaStream_t s);
-cudaError_t launch_correlate_sh2(int kx, const CUtensorMap& map, const CorrGeom& g,
-                                 const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
-                                 cudaStream_t s);
+#define NDC_DECL_CORR(SH, RY)                                                               \
+  cudaError_t launch_correlate_sh##SH##_ry##RY(int kx, const CUtensorMap& map,             \
+                                               const CorrGeom& g, const CorrArgs& a,       \
+                                               const TapBlock& taps, int batch, int nz_out, \
+                                               cudaStream_t s);
+NDC_DECL_CORR(0, 1)
+NDC_DECL_CORR(0, 2)
+NDC_DECL_CORR(2, 1)
+NDC_DECL_CORR(2, 2)
+#undef NDC_DECL_CORR
 size_t correlate_smem_bytes(const CorrGeom& g);
 int shared_pitch_for(int kx, int sh);
 

@@ -85,18 +85,38 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
                                   std::to_string(kMaxKX));
   if (kTileY + KY_ - 1 > kMaxRows)
     fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: kernel y-extent " + std::to_string(KY_) + " too large");
-  if (KY_ * KX_ > kTapCap)
+  if (KY_ * tap_pitch(KX_) > kTapCap)
     fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: one kernel z-slice exceeds the per-launch tap block");
   if (static_cast<long long>(my_) + 2 * py_ > (1 << 30) || static_cast<long long>(mx_) + 2 * px_ > (1 << 30))
     fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: extent too large");
+  // Two output rows per thread (tile height 128) halves the per-row tap loads and loop
+  // overhead; used for single-plane (2-D / batched) problems whose 128+KY-1 staged rows
+  // fit one TMA box.  3-D volumes keep 64-row tiles so two plane stages fit beside a
+  // second CTA per SM.
+  // For 3-D volumes two plane stages must also leave room for two CTAs per SM
+  // (measured: RY=2 wins on config 4's 21x9x9 PSF, loses on configs 3 and 5 whose
+  // 128-row stages would drop residency to one CTA).
+  stages_ = (KZ_ > 1) ? 2 : 1;
+  {
+    const long long pitch2 = std::max(shared_pitch_for(KX_, 0), shared_pitch_for(KX_, 2));
+    const long long stage2 = static_cast<long long>(2 * kTileY + KY_ - 1) * pitch2 * 4;
+    const bool fits = 2 * kTileY + KY_ - 1 <= kMaxRows;
+    ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= 90 * 1024)) ? 2 : 1;
+  }
+  if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
+  if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
 
-  // Taps: adjoint correlates with h, forward with flip(h) (kernel.hpp:41-45).
-  taps_adj_.resize(count);
-  taps_fwd_.resize(count);
+  // Taps: adjoint correlates with h, forward with flip(h) (kernel.hpp:41-45); each
+  // (kz, ky) row stored with the even pitch tap_pitch(KX) (zero pad).
+  const int kxp = tap_pitch(KX_);
+  const size_t rows = count / KX_;
+  taps_adj_.assign(rows * kxp, 0.0f);
+  taps_fwd_.assign(rows * kxp, 0.0f);
   kernel_all_zero_ = true;
   for (size_t i = 0; i < count; ++i) {
-    taps_adj_[i] = static_cast<float>(h[i]);
-    taps_fwd_[count - 1 - i] = static_cast<float>(h[i]);
+    const size_t j = count - 1 - i;  // flipped flat index
+    taps_adj_[(i / KX_) * kxp + i % KX_] = static_cast<float>(h[i]);
+    taps_fwd_[(j / KX_) * kxp + j % KX_] = static_cast<float>(h[i]);
     if (h[i] != 0.0) kernel_all_zero_ = false;
   }
 
@@ -171,7 +191,7 @@ float* Plan::dev_alloc_f(long long n) {
 long long Plan::partials_per_image(Dir d) const {
   const Vol& vo = (d == kFwd) ? Y_ : X_;
   const long long nz = (d == kFwd) ? (yb_ - ya_) : (xb_ - xa_);
-  return nz * cdiv(vo.ex, kTileX) * cdiv(vo.ey, kTileY);
+  return nz * cdiv(vo.ex, kTileX) * cdiv(vo.ey, kTileY * ry_);
 }
 
 void Plan::alloc_all() {
@@ -183,7 +203,7 @@ void Plan::alloc_all() {
   yobs_ = dev_alloc_f(ny);
   r_ = dev_alloc_f(ny);
   rt_ = dev_alloc_f(ny);
-  const int slices_per = kTapCap / (KY_ * KX_);
+  const int slices_per = kTapCap / (KY_ * tap_pitch(KX_));
   if (KZ_ > slices_per) scratch_ = dev_alloc_f(std::max(nx, ny));
   partials_cap_ = static_cast<long long>(B_) *
                   std::max({partials_per_image(kFwd), partials_per_image(kAdj),
@@ -218,7 +238,7 @@ const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh) {
   // x-shaped inputs are described including their zero margin (ndc_plan.h Vol)
   const CUresult rc = encode_tensor_map(&m, base, v.c0 + v.ex, v.r0 + v.ey,
                                         static_cast<long long>(v.ez) * B_, v.pitch, v.plane,
-                                        shared_pitch_for(KX_, sh), kTileY + KY_ - 1);
+                                        shared_pitch_for(KX_, sh), kTileY * ry_ + KY_ - 1);
   if (rc != CUDA_SUCCESS)
     fail(NDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
   return maps_.emplace(key, m).first->second;
@@ -234,6 +254,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   CorrGeom g{};
   g.in_ez = vin.ez;
   g.in_ey = vin.ey;
+  g.in_row0 = vin.r0;
   g.in_ex = vin.ex;
   g.out_ey = vout.ey;
   g.out_ex = vout.ex;
@@ -258,14 +279,14 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     fail(NDC_ERR_CUDA, "internal: negative or unaligned TMA tile origin");
   g.KY = KY_;
   g.tiles_x = static_cast<int>(cdiv(vout.ex, kTileX));
-  g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY));
-  g.rows = kTileY + KY_ - 1;
+  g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY * ry_));
+  g.rows = kTileY * ry_ + KY_ - 1;
   g.pitch_s = shared_pitch_for(KX_, sh);
   g.out_pitch = vout.pitch;
   g.out_plane = vout.plane;
   g.out_image = vout.image;
   g.mode = mode;
-  const int per_slice = KY_ * KX_;
+  const int per_slice = KY_ * tap_pitch(KX_);
   const int slices_per = kTapCap / per_slice;
   const int nchunks = static_cast<int>(cdiv(KZ_, slices_per));
   const CUtensorMap& map = map_for(in, d, sh);
@@ -273,7 +294,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   for (int c = 0; c < nchunks; ++c) {
     g.kz0 = c * slices_per;
     g.kz1 = std::min(KZ_, g.kz0 + slices_per);
-    g.stages = std::min(2, g.kz1 - g.kz0);
+    g.stages = std::min(stages_, g.kz1 - g.kz0);
     g.accum = c > 0;
     g.final_chunk = (c == nchunks - 1);
     // x-shaped operands are addressed from their interior origin
@@ -301,7 +322,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
       ev = ev_used_++;
       check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
     }
-    check_cuda(launch_correlate(KX_, sh, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
+    check_cuda(launch_correlate(KX_, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
                "correlate launch");
     if (timing_) {
       check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");

@@ -143,6 +143,8 @@ class Plan {
   size_t xext_[3] = {1, 1, 1}, kext_[3] = {1, 1, 1};
   int mz_ = 1, my_ = 1, mx_ = 1;
   int KZ_ = 1, KY_ = 1, KX_ = 1, pz_ = 0, py_ = 0, px_ = 0;
+  int ry_ = 1;      // output rows per thread in the correlation kernel (tile height 64*ry)
+  int stages_ = 1;  // TMA plane stages in flight per CTA
   std::vector<float> taps_fwd_, taps_adj_;
   bool kernel_all_zero_ = false;
 
