@@ -39,7 +39,7 @@ FFMA_PER_SM_CLK = 128
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
@@ -98,34 +98,54 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host arrival time, csv line)
+        self.window = None
 
-    def start(self):
+    def start(self, wait_first: float = 5.0):
+        """Start sampling every 50 ms; return once the first sample has arrived so the
+        timed region is covered (start it before the warm-up)."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + wait_first
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)  # let the sample after the window arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
+        sel = self.lines
+        basis = "all samples"
+        if self.window:
+            t0, t1 = self.window
+            inside = [l for l in self.lines if t0 <= l[0] <= t1 + 0.06]
+            if inside:
+                sel, basis = inside, "samples inside the timed region"
+            else:  # region shorter than the sampling period: nearest samples around it
+                near = sorted(self.lines, key=lambda l: min(abs(l[0] - t0), abs(l[0] - t1)))[:2]
+                sel, basis = near, "nearest samples to a timed region shorter than 50 ms"
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in sel:
             f = [s.strip() for s in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -138,7 +158,7 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "basis": basis}
 
 
 # --- inputs -----------------------------------------------------------------------------------
@@ -223,6 +243,8 @@ def run_ours(a):
     plan = nd.Plan(x_shape, h, batch=B, device=local)
     plan.set_observation(y)
     plan.pg_begin(cfg)
+    clocks = Clocks(local)
+    clocks.start()  # sampling runs through warm-up and the timed steps
     for _ in range(a.warmup):
         plan.pg_iterate(1)
     torch.cuda.set_device(local)
@@ -231,15 +253,15 @@ def run_ours(a):
     e1 = torch.cuda.Event(enable_timing=True)
     plan.reset_stats()
     plan.set_timing(True)
-    clocks = Clocks(local)
-    clocks.start()
     d.barrier()
     torch.cuda.synchronize()
+    t0 = time.time()
     e0.record(stream)
     for _ in range(a.steps):
         plan.pg_iterate(1)
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark(t0, time.time())
     d.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
