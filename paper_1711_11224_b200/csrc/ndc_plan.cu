@@ -106,19 +106,11 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
   if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
 
-  // Taps: adjoint correlates with h, forward with flip(h) (kernel.hpp:41-45); each
-  // (kz, ky) row stored with the even pitch tap_pitch(KX) (zero pad).
-  const int kxp = tap_pitch(KX_);
-  const size_t rows = count / KX_;
-  taps_adj_.assign(rows * kxp, 0.0f);
-  taps_fwd_.assign(rows * kxp, 0.0f);
+  h64_.assign(h, h + count);
+  set_taps(1.0);
   kernel_all_zero_ = true;
-  for (size_t i = 0; i < count; ++i) {
-    const size_t j = count - 1 - i;  // flipped flat index
-    taps_adj_[(i / KX_) * kxp + i % KX_] = static_cast<float>(h[i]);
-    taps_fwd_[(j / KX_) * kxp + j % KX_] = static_cast<float>(h[i]);
+  for (size_t i = 0; i < count; ++i)
     if (h[i] != 0.0) kernel_all_zero_ = false;
-  }
 
   // z-slab geometry: rank r owns x planes [xa, xb) and y planes
   // [xa+pz, xb+pz) (the first rank also [0, pz), the last up to mz+2pz).
@@ -782,9 +774,136 @@ void Plan::bench_adjoint() {
 }
 
 // ---- Richardson-Lucy (solvers.hpp:245-305) ----------------------------------------------
+// Taps: adjoint correlates with h, forward with flip(h) (kernel.hpp:41-45); each
+// (kz, ky) row stored with the even pitch tap_pitch(KX) (zero pad).
+void Plan::set_taps(double scale) {
+  const size_t count = h64_.size();
+  const int kxp = tap_pitch(KX_);
+  const size_t rows = count / KX_;
+  taps_adj_.assign(rows * kxp, 0.0f);
+  taps_fwd_.assign(rows * kxp, 0.0f);
+  for (size_t i = 0; i < count; ++i) {
+    const size_t j = count - 1 - i;  // flipped flat index
+    const float v = static_cast<float>(scale == 1.0 ? h64_[i] : h64_[i] * scale);
+    taps_adj_[(i / KX_) * kxp + i % KX_] = v;
+    taps_fwd_[(j / KX_) * kxp + j % KX_] = v;
+  }
+}
+
+// Richardson-Lucy (solvers.hpp:245-305) on the same operators: the kernel normalised to
+// unit sum, negative observations clamped (and counted), x0 = sum(yc)/n, then
+//   ratio = guarded_div(yc, A x)        forward pass, fused with r = Ax - yc, 0.5||r||^2
+//   kkt   = max|min(x, A^T r)|          adjoint pass (record, solvers.hpp:284-289)
+//   x'    = x .* A^T ratio, ||x'-x||, ||x||   adjoint pass (290-292)
+// per image, one 3-scalar D2H per iteration.
 void Plan::rl_run(const ndc_rl_config& c) {
-  (void)c;
-  fail(NDC_ERR_UNSUPPORTED, "deconv_rl: not wired in this build");
+  if (c.max_iters == 0) fail(NDC_ERR_CONFIG, "RlConfig: max_iters must be positive");
+  if (!(c.tol_rel_change >= 0)) fail(NDC_ERR_CONFIG, "RlConfig: tol_rel_change must be >= 0");
+  double hsum = 0.0;
+  for (double v : h64_) {
+    if (v < 0.0) fail(NDC_ERR_NUMERIC, "deconv_rl: kernel entries must be nonnegative");
+    hsum += v;
+  }
+  if (!(hsum > 0.0)) fail(NDC_ERR_NUMERIC, "deconv_rl: kernel must have positive sum");
+  wall0_ = now_s();
+  // hn = scale(h, 1/hsum) (solvers.hpp:256): multiply in f64 as the reference does
+  {
+    std::vector<double> hn(h64_.size());
+    for (size_t i = 0; i < hn.size(); ++i) hn[i] = h64_[i] * (1.0 / hsum);
+    std::swap(hn, h64_);
+    set_taps(1.0);
+    std::swap(hn, h64_);
+  }
+  struct Restore {
+    Plan* p;
+    ~Restore() { p->set_taps(1.0); }
+  } restore{this};
+
+  img_.assign(B_, Img{});
+  // yc = clamp(y), negatives counted, total = sum(yc)
+  const Geo yv = Y_.geo(yb_ - ya_);
+  float* yown = yobs_ + static_cast<long long>(ya_ - rlo_) * Y_.plane;
+  check_cuda(launch_clamp_count(yown, yown, partials_, static_cast<int>(B_), yv, kElemBlocks, stream_),
+             "clamp launch");
+  st_[2].launches++;
+  finalize(kElemBlocks, kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr, nullptr);
+  check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  sync();
+  halo_y(yobs_);
+  std::vector<double> total(B_);
+  std::vector<int> act(B_, 1);
+  const double n = static_cast<double>(mz_) * my_ * mx_;
+  for (size_t b = 0; b < B_; ++b) {
+    total[b] = hsc_[kAUX * B_ + b];
+    img_[b].clamped = static_cast<size_t>(hsc_[kCHG * B_ + b]);
+  }
+  // x0 per image: total/n, or 0 for an all-zero observation (solvers.hpp:263-270)
+  for (size_t b = 0; b < B_; ++b) {
+    const float v = total[b] > 0.0 ? static_cast<float>(total[b] / n) : 0.0f;
+    check_cuda(launch_fill(x_owned(x_) + b * X_.image, v, 1, X_.geo(xa_n_), stream_), "fill");
+    st_[2].launches++;
+  }
+  halo_x(x_);
+
+  auto record = [&](const std::vector<int>& a) {
+    // forward: ratio -> rt_, r -> r_, 0.5||r||^2 ; adjoint: kkt of x vs A^T r
+    upload_active(a);
+    correlate(kFwd, x_, rt_, kEpiRLRatio, r_, yobs_, nullptr, nullptr, dactive_, true);
+    finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kF * B_, nullptr, nullptr, dactive_);
+    halo_y(r_);
+    halo_y(rt_);
+    correlate(kAdj, r_, nullptr, kEpiKKT, nullptr, x_, nullptr, nullptr, dactive_, true);
+    finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
+             dactive_);
+    check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+    for (size_t b = 0; b < B_; ++b)
+      if (a[b]) {
+        img_[b].obj.push_back(hsc_[kF * B_ + b]);
+        img_[b].kkt.push_back(hsc_[kKKT * B_ + b]);
+      }
+  };
+  record(act);
+  for (size_t b = 0; b < B_; ++b)
+    if (!(total[b] > 0.0)) {
+      img_[b].reason = NDC_STOP_CONVERGED;
+      img_[b].active = false;
+      act[b] = 0;
+    }
+  for (size_t k = 1; k <= c.max_iters; ++k) {
+    size_t nact = 0;
+    for (size_t b = 0; b < B_; ++b) nact += act[b];
+    if (nact == 0) break;
+    upload_active(act);
+    // x' = x .* A^T ratio  (+ ||x'-x||^2, ||x||^2)
+    correlate(kAdj, rt_, trial_, kEpiRLUpdate, nullptr, x_, nullptr, nullptr, dactive_, true);
+    finalize(partials_per_image(kAdj), kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr,
+             dactive_);
+    check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+    std::vector<double> rel(B_, 0.0);
+    for (size_t b = 0; b < B_; ++b)
+      if (act[b])
+        rel[b] = std::sqrt(hsc_[kAUX * B_ + b]) / std::max(std::sqrt(hsc_[kCHG * B_ + b]), 1e-300);
+    std::swap(x_, trial_);
+    for (size_t b = 0; b < B_; ++b)
+      if (!act[b]) copy_image_x(x_, trial_, b);  // stopped images keep their iterate
+    halo_x(x_);
+    record(act);
+    for (size_t b = 0; b < B_; ++b) {
+      if (!act[b]) continue;
+      img_[b].iters = k;
+      if (rel[b] < c.tol_rel_change) {
+        img_[b].reason = NDC_STOP_CONVERGED;
+        img_[b].active = false;
+        act[b] = 0;
+      }
+    }
+  }
+  std::vector<int> all(B_, 1);
+  upload_active(all);
+  step0_ = 0.0;
+  wall_ = now_s() - wall0_;
 }
 
 }  // namespace ndc

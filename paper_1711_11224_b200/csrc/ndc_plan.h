@@ -146,6 +146,8 @@ class Plan {
   int ry_ = 1;      // output rows per thread in the correlation kernel (tile height 64*ry)
   int stages_ = 1;  // TMA plane stages in flight per CTA
   std::vector<float> taps_fwd_, taps_adj_;
+  std::vector<double> h64_;     // the kernel as given (f64, flat)
+  void set_taps(double scale);  // taps = float(h * scale), forward flipped, rows padded
   bool kernel_all_zero_ = false;
 
   // z-slab geometry (global plane indices); unsharded: one slab holding everything.

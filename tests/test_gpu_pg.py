@@ -193,3 +193,45 @@ def test_plan_stepping_equals_run(nd):
             r = p.report(b, 13)
             assert np.array_equal(est[b], full[b].estimate)
             assert np.array_equal(r.objective_trace, full[b].objective_trace)
+
+
+def test_rl_golden(nd, golden_solvers):
+    """deconv_rl (solvers.hpp:245-305) vs the reference's golden runs (7 iterations):
+    flux family (test_solvers.cpp:191-220) and the negative-data clamp count
+    (test_solvers.cpp:237-245)."""
+    d = golden_solvers
+    for i in range(int(d["nrl"])):
+        xs = tuple(int(v) for v in d[f"rl_xs{i}"])
+        rep = nd.deconv_rl(d[f"rl_y{i}"], d[f"rl_h{i}"], xs, nd.RlConfig(max_iters=7, tol_rel_change=0.0))
+        assert rel_l2(rep.estimate, d[f"rl_x{i}"]) <= 1e-5, i
+        np.testing.assert_allclose(rep.objective_trace, d[f"rl_obj{i}"], rtol=1e-4, atol=1e-9)
+        np.testing.assert_allclose(rep.kkt_trace, d[f"rl_kkt{i}"], rtol=1e-3, atol=1e-6)
+        assert rep.negative_pixels_clamped == int(d[f"rl_clamped{i}"])
+        assert rep.iterations_run == 7 and np.all(rep.estimate >= 0)
+
+
+def test_rl_kats(nd):
+    # test_solvers.cpp:180-189: delta kernel reproduces the data in one update
+    delta = np.array([0.0, 1.0, 0.0])
+    truth = np.array([1.0, 3.0, 0.5, 2.0])
+    rep = nd.deconv_rl(nd.conv_full(truth, delta), delta, (4,), nd.RlConfig(max_iters=1))
+    np.testing.assert_allclose(rep.estimate, truth, rtol=1e-6)
+    # flux conservation (test_solvers.cpp:191-220) at float32 resolution
+    g = np.random.Generator(np.random.PCG64(43))
+    h = g.uniform(0.05, 1.0, (3, 3))
+    x = g.uniform(0.05, 1.0, (5, 4))
+    y = nd.conv_full(x, h)
+    for iters in (1, 3, 7):
+        rep = nd.deconv_rl(y, h, x.shape, nd.RlConfig(max_iters=iters))
+        assert rep.iterations_run == iters
+        assert abs(rep.estimate.sum() - y.sum()) <= 1e-5 * abs(y.sum())
+    # rejects kernels it cannot normalise (test_solvers.cpp:246-255)
+    with pytest.raises(nd.NumericError):
+        nd.deconv_rl(np.zeros(6), [0.5, -0.1, 0.6], (4,))
+    with pytest.raises(nd.NumericError):
+        nd.deconv_rl(np.zeros(6), [0.0, 0.0, 0.0], (4,))
+    # relative-change stop (test_solvers.cpp:257-266)
+    hh = np.array([0.25, 0.5, 0.25])
+    tr = np.array([0.0, 1.0, 4.0, 4.0, 1.0, 0.0])
+    rep = nd.deconv_rl(nd.conv_full(tr, hh), hh, tr.shape, nd.RlConfig(max_iters=5000, tol_rel_change=1e-6))
+    assert rep.stop_reason == "converged" and rep.iterations_run < 5000
