@@ -7,6 +7,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 
 #include "ndc_plan.h"
 
@@ -168,16 +171,208 @@ Plan::~Plan() {
                   static_cast<void*>(dsc_), static_cast<void*>(dscale_),
                   static_cast<void*>(dactive_), static_cast<void*>(dstep_), static_cast<void*>(gather_),
                   staging_})
-    if (p) cudaFree(p);
-  if (hsc_) cudaFreeHost(hsc_);
+    if (p) cudaFreeAsync(p, stream_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  delete[] hsc_;
+  release_pinned();
   if (stream_) cudaStreamDestroy(stream_);
 }
 
-float* Plan::dev_alloc_f(long long n) {
+// Device memory comes from the device's stream-ordered pool with the release threshold
+// raised, so destroying and re-creating plans (every one-shot C-ABI call) reuses HBM
+// instead of paying cudaMalloc / cudaFree each time.
+void* Plan::dmalloc(size_t bytes) {
+  static bool pool_set[64] = {};
+  if (device_ < 64 && !pool_set[device_]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_set[device_] = true;
+  }
   void* p = nullptr;
-  check_cuda(cudaMalloc(&p, static_cast<size_t>(n) * 4), "cudaMalloc");
+  check_cuda(cudaMallocAsync(&p, bytes, stream_), "cudaMallocAsync");
+  return p;
+}
+
+float* Plan::dev_alloc_f(long long n) {
+  void* p = dmalloc(static_cast<size_t>(n) * 4);
   check_cuda(cudaMemsetAsync(p, 0, static_cast<size_t>(n) * 4, stream_), "cudaMemset");
   return static_cast<float*>(p);
+}
+
+namespace {
+// Persistent host copy pool: splits a pageable <-> pinned memcpy across worker threads
+// (a single thread moves ~10 GB/s; the PCIe DMA it feeds is several times faster).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t n) {
+    const unsigned parts = static_cast<unsigned>(std::min<size_t>(workers_.size() + 1, n >> 20));
+    if (parts <= 1) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    const size_t per = (n + parts - 1) / parts;
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel copy at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (unsigned i = 1; i < parts; ++i) {
+        const size_t lo = i * per, hi = std::min(n, lo + per);
+        if (lo < hi) {
+          jobs_.push_back({static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo});
+          ++pending_;
+        }
+      }
+    }
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(n, per));  // the caller takes part 0
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  struct Job {
+    char* dst;
+    const char* src;
+    size_t n;
+  };
+  CopyPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    for (unsigned i = 0; i + 1 < std::min(hw, 16u); ++i) workers_.emplace_back([this] { run(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void run() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+        if (stop_) return;
+        j = jobs_.back();
+        jobs_.pop_back();
+      }
+      std::memcpy(j.dst, j.src, j.n);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::vector<Job> jobs_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  size_t pending_ = 0;
+  bool stop_ = false;
+};
+
+void par_copy(void* dst, const void* src, size_t n) { CopyPool::get().copy(dst, src, n); }
+
+constexpr size_t kPinChunk = size_t(16) << 20;
+
+// Pinned staging rings are cached per process (cudaMallocHost / cudaFreeHost are slow
+// and would otherwise be paid by every one-shot call).
+struct PinnedRing {
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+std::mutex g_ring_mu;
+std::vector<PinnedRing> g_rings;
+}  // namespace
+
+void Plan::ensure_pinned() {
+  if (hpin_[0]) return;
+  PinnedRing r;
+  {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    if (!g_rings.empty()) {
+      r = g_rings.back();
+      g_rings.pop_back();
+    }
+  }
+  if (!r.buf[0]) {
+    for (int i = 0; i < 2; ++i) {
+      check_cuda(cudaMallocHost(&r.buf[i], kPinChunk), "cudaMallocHost staging");
+      check_cuda(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    hpin_[i] = r.buf[i];
+    pin_ev_[i] = r.ev[i];
+  }
+}
+
+void Plan::release_pinned() {
+  if (!hpin_[0]) return;
+  PinnedRing r;
+  for (int i = 0; i < 2; ++i) {
+    r.buf[i] = hpin_[i];
+    r.ev[i] = pin_ev_[i];
+    hpin_[i] = nullptr;
+    pin_ev_[i] = nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  g_rings.push_back(r);
+}
+
+// Host (pageable) -> device through a double-buffered pinned ring: host threads fill
+// one 16 MB slot while the DMA of the other runs.
+void Plan::h2d_staged(void* dev, const void* host, size_t bytes) {
+  if (bytes < (size_t(4) << 20)) {
+    check_cuda(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+    return;
+  }
+  ensure_pinned();
+  size_t i = 0;
+  for (size_t off = 0; off < bytes; off += kPinChunk, ++i) {
+    const int s = static_cast<int>(i & 1);
+    const size_t n = std::min(kPinChunk, bytes - off);
+    if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    par_copy(hpin_[s], static_cast<const char*>(host) + off, n);
+    check_cuda(cudaMemcpyAsync(static_cast<char*>(dev) + off, hpin_[s], n, cudaMemcpyHostToDevice,
+                               stream_),
+               "H2D");
+    check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
+  }
+}
+
+// Device -> host (pageable): the DMA of chunk i+1 overlaps the host copy-out of chunk i.
+void Plan::d2h_staged(void* host, const void* dev, size_t bytes) {
+  if (bytes < (size_t(4) << 20)) {
+    check_cuda(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+    sync();
+    return;
+  }
+  ensure_pinned();
+  const size_t nch = (bytes + kPinChunk - 1) / kPinChunk;
+  auto issue = [&](size_t i) {
+    const int s = static_cast<int>(i & 1);
+    const size_t off = i * kPinChunk, n = std::min(kPinChunk, bytes - off);
+    check_cuda(cudaMemcpyAsync(hpin_[s], static_cast<const char*>(dev) + off, n,
+                               cudaMemcpyDeviceToHost, stream_),
+               "D2H");
+    check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
+  };
+  if (nch == 0) return;
+  issue(0);
+  for (size_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch) issue(i + 1);
+    const int s = static_cast<int>(i & 1);
+    check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    const size_t off = i * kPinChunk, n = std::min(kPinChunk, bytes - off);
+    par_copy(static_cast<char*>(host) + off, hpin_[s], n);
+  }
 }
 
 long long Plan::partials_per_image(Dir d) const {
@@ -200,22 +395,22 @@ void Plan::alloc_all() {
   partials_cap_ = static_cast<long long>(B_) *
                   std::max({partials_per_image(kFwd), partials_per_image(kAdj),
                             static_cast<long long>(kElemBlocks)});
-  check_cuda(cudaMalloc(&partials_, partials_cap_ * sizeof(double2)), "cudaMalloc partials");
+  partials_ = static_cast<double2*>(dmalloc(partials_cap_ * sizeof(double2)));
   const size_t nsc = kNumSlots * B_ + kMaxPowerIters + 16;
-  check_cuda(cudaMalloc(&dsc_, nsc * sizeof(double)), "cudaMalloc scalars");
+  dsc_ = static_cast<double*>(dmalloc(nsc * sizeof(double)));
   check_cuda(cudaMemsetAsync(dsc_, 0, nsc * sizeof(double), stream_), "cudaMemset");
-  check_cuda(cudaMallocHost(&hsc_, nsc * sizeof(double)), "cudaMallocHost");
-  check_cuda(cudaMalloc(&dscale_, B_ * sizeof(float)), "cudaMalloc scale");
-  check_cuda(cudaMalloc(&dactive_, B_ * sizeof(int)), "cudaMalloc active");
-  check_cuda(cudaMalloc(&dstep_, B_ * sizeof(double)), "cudaMalloc step");
-  if (world_ > 1) check_cuda(cudaMalloc(&gather_, 2 * world_ * sizeof(double)), "cudaMalloc gather");
+  hsc_ = new double[nsc]();  // small scalar mirror (pageable: no cudaFreeHost on destroy)
+  dscale_ = static_cast<float*>(dmalloc(B_ * sizeof(float)));
+  dactive_ = static_cast<int*>(dmalloc(B_ * sizeof(int)));
+  dstep_ = static_cast<double*>(dmalloc(B_ * sizeof(double)));
+  if (world_ > 1) gather_ = static_cast<double*>(dmalloc(2 * world_ * sizeof(double)));
   std::vector<float> ones(B_, 1.0f);
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   std::vector<int> act(B_, 1);
   check_cuda(cudaMemcpyAsync(dactive_, act.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   staging_bytes_ = static_cast<size_t>(std::max(X_.ez * static_cast<long long>(X_.ey) * X_.ex,
                                                 Y_.ez * static_cast<long long>(Y_.ey) * Y_.ex)) * 8;
-  check_cuda(cudaMalloc(&staging_, staging_bytes_), "cudaMalloc staging");
+  staging_ = dmalloc(staging_bytes_);
   sync();
 }
 
@@ -400,8 +595,7 @@ void Plan::upload_active(const std::vector<int>& act) {
 void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 8, cudaMemcpyHostToDevice, stream_),
-               "H2D");
+    h2d_staged(staging_, host + b * per, per * 8);
     check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
                                dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
                                v.geo(nz), stream_),
@@ -414,8 +608,7 @@ void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_of
 void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(cudaMemcpyAsync(staging_, host + b * per, per * 4, cudaMemcpyHostToDevice, stream_),
-               "H2D");
+    h2d_staged(staging_, host + b * per, per * 4);
     check_cuda(launch_pack_f32(static_cast<const float*>(staging_),
                                dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
                                v.geo(nz), stream_),
@@ -432,9 +625,7 @@ void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_
                                  static_cast<double*>(staging_), 1, v.geo(nz), stream_),
                "unpack");
     st_[2].launches++;
-    check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 8, cudaMemcpyDeviceToHost, stream_),
-               "D2H");
-    sync();
+    d2h_staged(host + b * per, staging_, per * 8);
   }
 }
 
@@ -445,9 +636,7 @@ void Plan::unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_o
                                  static_cast<float*>(staging_), 1, v.geo(nz), stream_),
                "unpack");
     st_[2].launches++;
-    check_cuda(cudaMemcpyAsync(host + b * per, staging_, per * 4, cudaMemcpyDeviceToHost, stream_),
-               "D2H");
-    sync();
+    d2h_staged(host + b * per, staging_, per * 4);
   }
 }
 

@@ -113,7 +113,14 @@ class Plan {
  private:
   enum Dir { kFwd = 0, kAdj = 1 };
   void alloc_all();
+  void* dmalloc(size_t bytes);
   float* dev_alloc_f(long long n);
+  void ensure_pinned();
+  void release_pinned();
+  void h2d_staged(void* dev, const void* host, size_t bytes);
+  void d2h_staged(void* host, const void* dev, size_t bytes);
+  void* hpin_[2] = {nullptr, nullptr};      // pinned staging ring (16 MB slots)
+  cudaEvent_t pin_ev_[2] = {nullptr, nullptr};
   const CUtensorMap& map_for(const float* base, Dir d, int sh);
   // Correlation pass over resident buffers; mode / aux per EpiMode.
   void correlate(Dir d, const float* in, float* out, int mode, float* aux_out, const float* aux_in,
