@@ -39,7 +39,7 @@ FFMA_PER_SM_CLK = 128
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None, help="timed PG iterations (default per config)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
@@ -161,71 +161,96 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm), "basis": basis}
 
 
-# --- inputs -----------------------------------------------------------------------------------
+# --- workloads --------------------------------------------------------------------------------
 
-def inputs(config: str, rank: int):
+# Per-config defaults: iterations per e2e call, timed steps, explicit step size.  Configs
+# 4/5 use initial_step = 1 (their PSFs are nonnegative with unit sum, so ||A|| <= 1 and
+# 1 is a valid gradient step; it skips a power iteration costing 60 passes = 30 PG
+# iterations of compute); configs 2/3 estimate the step (untimed setup).
+WORK = {
+    "c2": dict(e2e_iters=100, steps=30, step=None, desc="16x2048x2048 2D batch, PSF 31x31 sigma 4, Poisson 1000"),
+    "c3": dict(e2e_iters=50, steps=20, step=None, desc="3D 256x256x128, PSF 15x15x31 sigma_xy 1.5 sigma_z 4"),
+    "c4": dict(e2e_iters=4, steps=5, step=1.0, desc="3D 1024x1024x512, PSF 9x9x21, Poisson 500"),
+    "c5": dict(e2e_iters=2, steps=2, step=1.0, desc="3D 2048x2048x256, 33x33x65 3-Gaussian PSF, Poisson 200"),
+}
+
+
+def inputs(config: str, rank: int, sharded: bool):
+    """x (B, ...), y (B, ...) float32-exact and the PSF.  2-D batches get a different
+    seed per rank (independent replicas); a sharded 3-D volume is the same on every rank
+    (each keeps its own z-slab)."""
     from paper_1711_11224_b200 import synth
-    x, y, h = synth.make(config, seed=synth.SEED + 100003 * rank)
+    seed = synth.SEED if sharded else synth.SEED + 100003 * rank
+    x, y, h = synth.make(config, seed=seed)
     if x.ndim == len(h.shape):  # single volume -> batch of one
         x, y = x[None], y[None]
     return x.astype(np.float32), y.astype(np.float32), h
 
 
-def algorithmic(config: str, batch: int, x_shape, h):
-    K = int(np.prod(h.shape))
-    voxels = batch * int(np.prod(x_shape))
-    y_vox = batch * int(np.prod([a + b - 1 for a, b in zip(x_shape, h.shape)]))
-    rho = y_vox / voxels
-    return K, voxels, rho
-
-
 # --- CPU baseline (reference compiled from /root/reference: oracle/_ref) --------------------
 
-def cpu_reference_sample(config: str, iters: int, warm: int = 0):
-    """Time `iters` PG iterations of the reference's own operators (ref_pg_iterations,
-    solvers.hpp:179-228 loop body) on ONE image of the config, all host threads."""
-    from oracle.oracle import Oracle, available
-    kind = "reference" if available("ref") else "port"
-    orc = Oracle("ref" if kind == "reference" else "c")
-    cores = os.cpu_count() or 1
-    orc.set_threads(cores)
-    from paper_1711_11224_b200 import synth
-    if config in ("c1", "c2"):
-        x, y, h = synth.make(config, batch=1) if config == "c2" else (None, None, None)
+class RefRunner:
+    """The reference's own CPU path on ONE image of the config (configs 3-5: a reduced
+    volume with the same PSF), all host threads.  setup() builds A^T y, x0 and
+    A x0 untimed; step() times one PG loop-body iteration (ref_pg_iterations = the
+    reference's operators in solvers.hpp:179-228 order)."""
+
+    def __init__(self, config: str):
+        from oracle.oracle import Oracle, available
+        from paper_1711_11224_b200 import synth
+        self.kind = "reference" if available("ref") else "port"
+        self.orc = Oracle("ref" if self.kind == "reference" else "c")
+        self.cores = os.cpu_count() or 1
+        self.orc.set_threads(self.cores)
         if config == "c2":
-            y = y[0]
-            xs = (2048, 2048)
+            _, y, h = synth.make("c2", batch=1)
+            self.y, self.h, self.xs = y[0], h, (2048, 2048)
+        elif config == "c1":
+            x, self.y, self.h = synth.make("c1")
+            self.xs = x.shape
         else:
-            x, y, h = synth.make("c1")
-            xs = x.shape
-        sample = f"1 image {xs[0]}x{xs[1]}, PSF {h.shape}"
-    else:
-        # reduced xy crop of the 3D configs with the same PSF (SURVEY §8d)
-        shape = {"c3": (128, 256, 256), "c4": (64, 128, 128), "c5": (64, 96, 96)}[config]
-        x, y, h = synth.make(config, shape=shape, n_objects=200)
-        xs = x.shape
-        sample = f"volume {xs}, PSF {h.shape}"
-    step0 = 1.0  # unit-sum PSFs: lambda_max(A^T A) <= 1; the loop body cost is step-independent
-    if kind == "reference":
-        aty = orc.adjoint_apply(y, h, xs)
-        xk = np.maximum(aty, 0.0)
-        ax = orc.conv_full(xk, h)
-        f = 0.5 * float(np.sum((ax - y) ** 2))
-        if warm:
-            f, _ = orc.pg_iterations(y, h, xs, step0, warm, xk, ax, aty, f)
+            shape = {"c3": (128, 256, 256), "c4": (64, 128, 128), "c5": (64, 96, 96)}[config]
+            x, self.y, self.h = synth.make(config, shape=shape, n_objects=200)
+            self.xs = x.shape
+        self.sample = f"{'1 image' if config in ('c1', 'c2') else 'volume'} {self.xs}, PSF {self.h.shape}"
+        self.voxels = int(np.prod(self.xs))
+        self.step0 = 1.0  # unit-sum PSFs: ||A|| <= 1; loop-body cost does not depend on it
+
+    def setup(self):
+        self.aty = self.orc.adjoint_apply(self.y, self.h, self.xs)
+        self.x = np.maximum(self.aty, 0.0)
+        self.ax = self.orc.conv_full(self.x, self.h)
+        self.f = 0.5 * float(np.sum((self.ax - self.y) ** 2))
+
+    def step(self, iters: int = 1) -> float:
         t0 = time.perf_counter()
-        f, acc = orc.pg_iterations(y, h, xs, step0, iters, xk, ax, aty, f)
-        dt = time.perf_counter() - t0
-    else:
-        t0 = time.perf_counter()
-        orc.deconv_pg(y, h, xs, max_iters=iters, tol_rel_objective=0.0, initial_step=step0)
-        dt = time.perf_counter() - t0
-    vox = int(np.prod(xs))
-    return {"value": vox * iters / dt, "unit": "voxel-iterations/s", "cores": cores, "kind": kind,
-            "sample": f"{sample}, {iters} PG iterations (loop body only), {dt:.2f} s"}, dt
+        if self.kind == "reference":
+            self.f, _ = self.orc.pg_iterations(self.y, self.h, self.xs, self.step0, iters, self.x, self.ax,
+                                               self.aty, self.f)
+        else:
+            self.orc.deconv_pg(self.y, self.h, self.xs, max_iters=iters, tol_rel_objective=0.0,
+                               initial_step=self.step0)
+        return time.perf_counter() - t0
+
+
+def cpu_reference_sample(config: str, iters: int):
+    r = RefRunner(config)
+    r.setup()
+    dt = r.step(iters)
+    return {"value": r.voxels * iters / dt, "unit": "voxel-iterations/s", "cores": r.cores, "kind": r.kind,
+            "sample": f"{r.sample}, {iters} PG iterations (loop body only), {dt:.2f} s"}, dt
 
 
 # --- our arm ------------------------------------------------------------------------------------
+
+def make_plan(nd, d, x_shape, h, B, local, sharded):
+    if not sharded:
+        return nd.Plan(x_shape, h, batch=B, device=local)
+    uid = nd.nccl_unique_id() if d.rank == 0 else None
+    obj = [uid]
+    d.dist.broadcast_object_list(obj, src=0)
+    return nd.Plan.sharded(x_shape, h, d.rank, d.world, obj[0], device=local)
+
 
 def run_ours(a):
     rank, world, local = dist_env()
@@ -234,14 +259,22 @@ def run_ours(a):
     from paper_1711_11224_b200 import ndconv as nd
     if nd.device_count() < 1:
         raise SystemExit("no B200 visible")
-    x, y, h = inputs(a.config, rank)
+    work = WORK[a.config]
+    steps = a.steps if a.steps is not None else work["steps"]
+    sharded = world > 1 and a.config in ("c3", "c4", "c5")
+    x, y, h = inputs(a.config, rank, sharded)
     B = y.shape[0]
     x_shape = x.shape[1:]
-    K, voxels, rho = algorithmic(a.config, B, x_shape, h)
-    cfg = nd.DeconvConfig(max_iters=a.warmup + a.steps + 1, tol_rel_objective=0.0)
+    K = int(np.prod(h.shape))
+    plan = make_plan(nd, d, x_shape, h, B, local, sharded)
+    ya, yb = plan.y_range
+    xa, xb = plan.x_range
+    y_own = y[:, ya:yb] if sharded else y
+    vox_rank = B * (xb - xa) * int(np.prod(x_shape[1:])) if sharded else B * int(np.prod(x_shape))
+    vox_job = B * int(np.prod(x_shape)) * (1 if sharded else world)
+    cfg = nd.DeconvConfig(max_iters=a.warmup + steps + 1, tol_rel_objective=0.0, initial_step=work["step"])
 
-    plan = nd.Plan(x_shape, h, batch=B, device=local)
-    plan.set_observation(y)
+    plan.set_observation(y_own)
     plan.pg_begin(cfg)
     clocks = Clocks(local)
     clocks.start()  # sampling runs through warm-up and the timed steps
@@ -257,7 +290,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     t0 = time.time()
     e0.record(stream)
-    for _ in range(a.steps):
+    for _ in range(steps):
         plan.pg_iterate(1)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -274,13 +307,16 @@ def run_ours(a):
     rep = plan.report(0, cfg.max_iters + 1)
     plan.close()
 
-    value = world * voxels * a.steps / (ms_max / 1e3)
-    # dominant kernel roofline: algorithmic FLOPs per launch = 2 K per x voxel (forward:
-    # every x voxel meets K taps; adjoint: every output meets K taps)
-    flops_launch = 2.0 * K * voxels
+    value = vox_job * steps / (ms_max / 1e3)
+    # Dominant kernel: algorithmic FLOPs per pass = 2 K per x voxel of this rank (forward:
+    # every x voxel meets K taps; adjoint: every output meets K taps).  A pass is one
+    # launch, or several tap-chunk launches for PSFs beyond the 7680-tap parameter block
+    # (config 5) -- the roofline uses the pass time.
+    flops_pass = 2.0 * K * vox_rank
+    passes = steps  # one forward and one adjoint per accepted iteration without backtracks
     dom, n_dom, ms_dom = ("adjoint", n_adj, ms_adj) if ms_adj >= ms_fwd else ("forward", n_fwd, ms_fwd)
-    avg_s = ms_dom / max(n_dom, 1) / 1e3
-    achieved = flops_launch / avg_s / 1e12
+    avg_s = ms_dom / max(passes, 1) / 1e3
+    achieved = flops_pass / avg_s / 1e12
     smax = clk.get("sm_max_mhz") or 1965.0
     peak = N_SM * FFMA_PER_SM_CLK * 2 * smax * 1e6 / 1e12
     traffic = None
@@ -292,21 +328,23 @@ def run_ours(a):
             traffic = None
     line = {
         "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
-        "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{a.config}: 16x2048x2048 2D batch, PSF 31x31 sigma 4, Poisson 1000"
-                   if a.config == "c2" else a.config,
+        "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": steps,
+        "warmup": a.warmup, "ms_per_step": ms_max / steps, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{a.config}: {work['desc']}",
                    "batch_per_gpu": B, "x_shape": list(x_shape), "psf": list(h.shape), "taps": K,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"z-slab{world}" if sharded else f"replicas{world}") if world > 1 else "single",
                    "l2": "inputs larger than L2 (no flush)", "step": "one PG iteration over the batch",
-                   "tol_rel_objective": 0.0, "step_size": "auto (power iteration, untimed setup)"},
+                   "tol_rel_objective": 0.0,
+                   "step_size": "auto (power iteration, untimed setup)" if work["step"] is None
+                   else f"initial_step={work['step']} (unit-sum PSF)"},
         "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_basis": f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (sm max clock); "
                                    "no measured FP32 peak in MEASURED_PEAKS.json",
-                     "algorithmic_flops_per_launch": flops_launch,
-                     "launch_ms": avg_s * 1e3,
+                     "algorithmic_flops_per_pass": flops_pass, "pass_ms": avg_s * 1e3,
+                     "launches_per_pass": n_dom / max(passes, 1),
                      "frac_at_observed_clock": (achieved / (N_SM * FFMA_PER_SM_CLK * 2 * clk["sm_mhz"] * 1e6 / 1e12)
                                                 if clk.get("sm_mhz") else None),
                      "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}},
@@ -315,8 +353,8 @@ def run_ours(a):
         "iterations_accepted": int(rep.iterations_run),
         "backtracks": int(rep.extra.get("backtracks", 0)),
     }
-    if not a.no_e2e:
-        line["e2e"] = e2e(a, nd, y, h, x_shape, B, voxels, world, d)
+    if not a.no_e2e and not sharded:
+        line["e2e"] = e2e(a, nd, y, h, x_shape, B, work, world, d)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cb, _ = cpu_reference_sample(a.config, a.cpu_iters)
         line["cpu_baseline"] = cb
@@ -325,19 +363,19 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
 
 
-def e2e(a, nd, y32, h, x_shape, B, voxels, world, d):
-    """Public C-ABI call (ndc_deconv_pg_batch_f64) with host f64 buffers: the whole
-    config-2 solve (auto step, 100 iterations) per step, copies included."""
+def e2e(a, nd, y32, h, x_shape, B, work, world, d):
+    """Public C-ABI call (ndc_deconv_pg_batch_f64) with host f64 buffers: a whole solve
+    per step -- H2D of Y, step estimate, all iterations, D2H of estimate and traces."""
     import ctypes as C
     from paper_1711_11224_b200 import _native as N
-    iters = 100 if a.config == "c2" else 20
+    iters = work["e2e_iters"]
     yh = np.ascontiguousarray(y32, dtype=np.float64)
     xo = np.empty((B,) + tuple(x_shape), np.float64)
     cap = iters + 1
     obj = np.empty((B, cap))
     kkt = np.empty((B, cap))
     reps = (N.Report * B)()
-    cfg = nd.DeconvConfig(max_iters=iters, tol_rel_objective=0.0).to_c()
+    cfg = nd.DeconvConfig(max_iters=iters, tol_rel_objective=0.0, initial_step=work["step"]).to_c()
     ext = (C.c_size_t * len(x_shape))(*x_shape)
     yext = (C.c_size_t * len(x_shape))(*yh.shape[1:])
     hext = (C.c_size_t * h.ndim)(*h.shape)
@@ -359,35 +397,38 @@ def e2e(a, nd, y32, h, x_shape, B, voxels, world, d):
         call()
         reps_t.append(time.perf_counter() - t0)
     dt = d.max(min(reps_t))
+    voxels = B * int(np.prod(x_shape))
     return {"value": world * voxels * iters / dt, "unit": "voxel-iterations/s",
             "h2d_bytes_per_step": int(yh.nbytes + hh.nbytes), "d2h_bytes_per_step": int(xo.nbytes + obj.nbytes + kkt.nbytes),
-            "step": f"one full deconv_pg_batch_f64 call: {B} images, {iters} iterations, auto step",
+            "step": f"one full deconv_pg_batch_f64 call: {B} image(s), {iters} iterations, "
+                    + ("auto step" if work["step"] is None else f"initial_step={work['step']}"),
             "seconds_per_step": dt}
 
 
 def run_reference(a):
+    """The reference's CPU implementation on the box's host cores (oracle/_ref: the
+    unmodified reference headers compiled by oracle/Makefile), same config and metric;
+    rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cb = None
-    times = []
-    warm_total = 0.0
-    for i in range(a.warmup + a.steps):
-        cb, dt = cpu_reference_sample(a.config, 1)
-        if i >= a.warmup:
-            times.append(dt)
-        else:
-            warm_total += dt
+    steps = a.steps if a.steps is not None else 10
+    r = RefRunner(a.config)
+    r.setup()
+    for _ in range(a.warmup):
+        r.step(1)
+    times = [r.step(1) for _ in range(steps)]
     per = float(np.sum(times))
-    vox = 2048 * 2048 if a.config == "c2" else None
-    value = cb["value"] if vox is None else vox * a.steps / per
-    cb = dict(cb, value=value, sample=cb["sample"].rsplit(",", 1)[0] + f", {a.steps} timed steps of 1 PG iteration")
+    value = r.voxels * steps / per
+    cb = {"value": value, "unit": "voxel-iterations/s", "cores": r.cores, "kind": r.kind,
+          "sample": f"{r.sample}, {steps} timed steps of 1 PG iteration (loop body), {per:.2f} s"}
     line = {
         "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
         "impl": "reference", "value": value, "unit": "voxel-iterations/s", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": per / a.steps * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": a.warmup, "ms_per_step": per / steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{a.config} (reference CPU path, 1 image per step)", "parallelism": "cpu threads"},
+        "config": {"workload": f"{a.config}: {WORK[a.config]['desc']} (reference CPU path, "
+                               f"{r.sample} per step)", "parallelism": f"{r.cores} cpu threads"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
