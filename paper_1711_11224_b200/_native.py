@@ -8,7 +8,9 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libndconv_b200.so")
+# NDC_LIB_PATH overrides the in-tree library (kernel-variant experiments in tools/).
+LIB_PATH = os.environ.get("NDC_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libndconv_b200.so")
 
 size_t_p = C.POINTER(C.c_size_t)
 dbl_p = C.POINTER(C.c_double)

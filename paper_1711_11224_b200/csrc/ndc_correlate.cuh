@@ -207,7 +207,11 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
   // (LDCU -> FFMA R, R, UR).
   for (int ky = 0; ky < KY; ++ky) {
     const float* w = trow + ky * KXP;
+#if defined(NDC_J_NOUNROLL)
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
     for (int j = 0; j < NR; ++j) {
       const float* rp = base + (ky + 32 * j) * pitch_s;
       float win[NQ * 4];
@@ -229,12 +233,14 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
   }
 }
 
+#ifndef NDC_MIN_BLOCKS
+#define NDC_MIN_BLOCKS 2
+#endif
 template <int KX, int SH, int RY>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
     correlate_kernel(const __grid_constant__ CUtensorMap map, const CorrGeom g, const CorrArgs a,
                      const __grid_constant__ TapBlock taps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double red0[kThreads / 32], red1[kThreads / 32];
   constexpr int TY = 64 * RY;
 
   const int b = blockIdx.z;
@@ -301,12 +307,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       accumulate_rows<KX, SH, RY, RY>(acc, base, trow, g.KY, g.pitch_s);
     else if (RY > 1 && nrun == 1)
       accumulate_rows<KX, SH, RY, 1>(acc, base, trow, g.KY, g.pitch_s);
-    __syncthreads();  // every warp is done with stage s
-    if (tid == 0 && i + g.stages < n) {
-      const int iz = oz + kzA + i + g.stages + g.off_z;
-      mbar_expect_tx(&bars[s], tx_bytes);
-      tma_load_3d(smem_raw + s * sbytes, &map, &bars[s], tx0 + g.off_x, ty0 + g.off_y,
-                  b * g.in_ez + iz);
+    if (i + g.stages < n) {
+      __syncthreads();  // every warp is done with stage s before it is refilled
+      if (tid == 0) {
+        const int iz = oz + kzA + i + g.stages + g.off_z;
+        mbar_expect_tx(&bars[s], tx_bytes);
+        tma_load_3d(smem_raw + s * sbytes, &map, &bars[s], tx0 + g.off_x, ty0 + g.off_y,
+                    b * g.in_ez + iz);
+      }
     }
   }
 
@@ -325,23 +333,16 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 
   if (a.partials != nullptr) {
+    // one partial per warp, written without a CTA barrier (finalize reduces them in a
+    // fixed order, so the result stays deterministic)
     const bool pmax = p0_is_max(g.mode);
     p0 = pmax ? warp_max(p0) : warp_sum(p0);
     p1 = warp_sum(p1);
     if (lane == 0) {
-      red0[warp] = p0;
-      red1[warp] = p1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double s0 = red0[0], s1 = red1[0];
-      for (int w = 1; w < kThreads / 32; ++w) {
-        s0 = pmax ? fmax(s0, red0[w]) : s0 + red0[w];
-        s1 += red1[w];
-      }
       const long long idx =
-          (static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile;
-      a.partials[idx] = make_double2(s0, s1);
+          ((static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile) *
+              (kThreads / 32) + warp;
+      a.partials[idx] = make_double2(p0, p1);
     }
   }
 }

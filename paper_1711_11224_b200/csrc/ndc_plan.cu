@@ -378,7 +378,7 @@ void Plan::d2h_staged(void* host, const void* dev, size_t bytes) {
 long long Plan::partials_per_image(Dir d) const {
   const Vol& vo = (d == kFwd) ? Y_ : X_;
   const long long nz = (d == kFwd) ? (yb_ - ya_) : (xb_ - xa_);
-  return nz * cdiv(vo.ex, kTileX) * cdiv(vo.ey, kTileY * ry_);
+  return nz * cdiv(vo.ex, kTileX) * cdiv(vo.ey, kTileY * ry_) * (kThreads / 32);  // per warp
 }
 
 void Plan::alloc_all() {
