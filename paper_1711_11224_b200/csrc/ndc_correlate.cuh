@@ -200,12 +200,16 @@ __device__ __forceinline__ void epilogue_strip(const CorrGeom& g, const CorrArgs
 // NR of the thread's RY row windows against every tap row of one staged plane.
 template <int KX, int SH, int RY, int NR>
 __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const float* base,
-                                                const float* trow, int KY, int pitch_s) {
+                                                const float* trow, int KY, int kyA, int kyB,
+                                                int pitch_s) {
   constexpr int NQ = window_quads(KX, SH);
   constexpr int KXP = tap_pitch(KX);
   // ky from 0: a uniform induction variable keeps the tap loads on the uniform datapath
-  // (LDCU -> FFMA R, R, UR).
+  // (LDCU -> FFMA R, R, UR); [kyA, kyB) is warp-uniform (see the caller).
   for (int ky = 0; ky < KY; ++ky) {
+#if defined(NDC_KY_SKIP)
+    if (ky < kyA || ky >= kyB) continue;
+#endif
     const float* w = trow + ky * KXP;
 #if defined(NDC_J_NOUNROLL)
 #pragma unroll 1
@@ -297,6 +301,19 @@ __global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
   for (int j = 0; j < RY; ++j)
     if (ty0 + wy * (32 * RY) + 32 * j < g.out_ey) nrun = j + 1;
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
+  // Tap rows whose input row lies outside the data for every row this warp computes
+  // multiply only zero fill (forward pass near the y borders).  Data row of (output row
+  // r, tap row ky) = r + ky + off_y - in_row0.
+  int kyA = 0, kyB = g.KY;
+#if defined(NDC_KY_SKIP)
+  {
+    const int rw = ty0 + wy * (32 * RY);
+    const int dd = g.off_y - g.in_row0;
+    const int span = 32 * (nrun > 0 ? nrun : 1);
+    kyA = max(0, -dd - rw - span + 1);
+    kyB = min(g.KY, g.in_ey - dd - rw);
+  }
+#endif
   for (int i = 0; i < n; ++i) {
     const int s = i % g.stages;
     mbar_wait(&bars[s], static_cast<uint32_t>((i / g.stages) & 1));
@@ -304,9 +321,9 @@ __global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
         reinterpret_cast<const float*>(smem_raw + s * sbytes) + row_l * g.pitch_s + wx * kRX;
     const float* trow = taps.t + (kzA + i - g.kz0) * g.KY * tap_pitch(KX);
     if (nrun == RY)
-      accumulate_rows<KX, SH, RY, RY>(acc, base, trow, g.KY, g.pitch_s);
+      accumulate_rows<KX, SH, RY, RY>(acc, base, trow, g.KY, kyA, kyB, g.pitch_s);
     else if (RY > 1 && nrun == 1)
-      accumulate_rows<KX, SH, RY, 1>(acc, base, trow, g.KY, g.pitch_s);
+      accumulate_rows<KX, SH, RY, 1>(acc, base, trow, g.KY, kyA, kyB, g.pitch_s);
     if (i + g.stages < n) {
       __syncthreads();  // every warp is done with stage s before it is refilled
       if (tid == 0) {
