@@ -124,6 +124,12 @@ cudaError_t launch_pg_trial(const float* x, const float* g, float* trial, const 
                             const int* active, double2* partials, int batch, const Geo& v,
                             int blocks_per_image, cudaStream_t s);
 cudaError_t launch_fill(float* dst, float value, int batch, const Geo& v, cudaStream_t s);
+// float64 dense correlation (small-problem reference-exact power iteration)
+cudaError_t launch_corr_f64(const double* in, int iz, int iy, int ix, double* out, int oz, int oy,
+                            int ox, const double* taps, int KZ, int KY, int KX, int dz, int dy,
+                            int dx, const double* lam_prev, double2* partials, long long* nblocks,
+                            cudaStream_t s);
+cudaError_t launch_fill_f64(double* dst, double value, long long n, cudaStream_t s);
 cudaError_t launch_pack_f64(const double* dense, float* pitched, int batch, const Geo& v,
                             cudaStream_t s);
 cudaError_t launch_unpack_f64(const float* pitched, double* dense, int batch, const Geo& v,

@@ -177,6 +177,54 @@ __global__ void clamp_count_kernel(const float* __restrict__ src, float* __restr
   }
 }
 
+// float64 direct correlation for small problems (the reference-exact power iteration,
+// solvers.hpp:127-143): one output per thread, dense [z][y][x] f64 buffers, taps in
+// global memory, input zero outside its extents.  out = acc / lam_prev (1 if null);
+// with `partials`, per-block sum of out^2 (fixed order).
+__global__ void corr_f64_kernel(const double* __restrict__ in, int iz, int iy, int ix,
+                                double* __restrict__ out, int oz, int oy, int ox,
+                                const double* __restrict__ taps, int KZ, int KY, int KX, int dz,
+                                int dy, int dx, const double* lam_prev, double2* partials) {
+  __shared__ double red[32];
+  const long long n = static_cast<long long>(oz) * oy * ox;
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    const int x = static_cast<int>(i % ox);
+    const int y = static_cast<int>((i / ox) % oy);
+    const int z = static_cast<int>(i / (static_cast<long long>(ox) * oy));
+    const int z0 = z + dz, y0 = y + dy, x0 = x + dx;
+    const int kza = max(0, -z0), kzb = min(KZ, iz - z0);
+    const int kya = max(0, -y0), kyb = min(KY, iy - y0);
+    const int kxa = max(0, -x0), kxb = min(KX, ix - x0);
+    double acc = 0.0;
+    for (int kz = kza; kz < kzb; ++kz)
+      for (int ky = kya; ky < kyb; ++ky) {
+        const double* ip = in + (static_cast<long long>(z0 + kz) * iy + (y0 + ky)) * ix + x0;
+        const double* tp = taps + (static_cast<long long>(kz) * KY + ky) * KX;
+        for (int kx = kxa; kx < kxb; ++kx) acc = fma(tp[kx], ip[kx], acc);
+      }
+    v = (lam_prev != nullptr) ? acc * (1.0 / *lam_prev) : acc;
+    out[i] = v;
+  }
+  if (partials != nullptr) {
+    double s = warp_sum(v * v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += red[w];
+      partials[blockIdx.x] = make_double2(t, 0.0);
+    }
+  }
+}
+
+__global__ void fill_f64_kernel(double* dst, double value, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = value;
+}
+
 __global__ void fill_kernel(float* dst, float value, Geo v) {
   const int b = blockIdx.y;
   for (long long r = blockIdx.x; r < static_cast<long long>(v.ez) * v.ey; r += gridDim.x) {
@@ -257,6 +305,24 @@ cudaError_t launch_clamp_count(const float* src, float* dst, double2* partials, 
                                const Geo& v, int blocks_per_image, cudaStream_t s) {
   dim3 grid(blocks_per_image, batch);
   clamp_count_kernel<<<grid, 256, 0, s>>>(src, dst, partials, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_corr_f64(const double* in, int iz, int iy, int ix, double* out, int oz, int oy,
+                            int ox, const double* taps, int KZ, int KY, int KX, int dz, int dy,
+                            int dx, const double* lam_prev, double2* partials, long long* nblocks,
+                            cudaStream_t s) {
+  const long long n = static_cast<long long>(oz) * oy * ox;
+  const long long nb = (n + 255) / 256;
+  if (nblocks) *nblocks = nb;
+  corr_f64_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(in, iz, iy, ix, out, oz, oy, ox, taps, KZ,
+                                                            KY, KX, dz, dy, dx, lam_prev, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_f64(double* dst, double value, long long n, cudaStream_t s) {
+  fill_f64_kernel<<<static_cast<unsigned>(std::min<long long>((n + 255) / 256, 4096)), 256, 0, s>>>(dst, value,
+                                                                                               n);
   return cudaGetLastError();
 }
 

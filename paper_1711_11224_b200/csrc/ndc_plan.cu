@@ -703,6 +703,11 @@ double Plan::estimate_step(size_t power_iters) {
     fail(NDC_ERR_UNSUPPORTED, "estimate_step: power_iters too large");
   if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "estimate_step: degenerate all-zero kernel");
   const double n = static_cast<double>(mz_) * my_ * mx_;
+  // Small problems run the power iteration in float64: when all-ones is an exact but
+  // non-dominant eigenvector of A^T A (symmetric tiny shapes), the reference's f64
+  // iteration stays in that eigenspace and float32 rounding would not.
+  if (world_ == 1 && n * static_cast<double>(h64_.size()) <= static_cast<double>(1 << 28))
+    return estimate_step_f64(power_iters);
   const size_t saveB = B_;
   // image 0 only: launch with batch 1 (buffers are laid out image-major)
   B_ = 1;
@@ -736,6 +741,53 @@ double Plan::estimate_step(size_t power_iters) {
   std::vector<float> ones(B_, 1.0f);
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   sync();
+  return 1.0 / hsc_[power_iters - 1];
+}
+
+// solvers.hpp:127-143 in float64 on dense scratch buffers (small problems only).
+double Plan::estimate_step_f64(size_t power_iters) {
+  const long long nx = static_cast<long long>(mz_) * my_ * mx_;
+  const int oz = mz_ + 2 * pz_, oy = my_ + 2 * py_, ox = mx_ + 2 * px_;
+  const long long ny = static_cast<long long>(oz) * oy * ox;
+  const size_t K = h64_.size();
+  std::vector<double> hf(h64_.rbegin(), h64_.rend());  // flip (kernel.hpp:41-45)
+  double* dh = static_cast<double*>(dmalloc(K * 8));
+  double* dhf = static_cast<double*>(dmalloc(K * 8));
+  double* v = static_cast<double*>(dmalloc(nx * 8));
+  double* u = static_cast<double*>(dmalloc(ny * 8));
+  const long long nbx = (nx + 255) / 256;
+  double2* part = static_cast<double2*>(dmalloc(nbx * sizeof(double2)));
+  double* lam = dsc_ + kNumSlots * B_;
+  struct Free {
+    Plan* p;
+    void* q[5];
+    ~Free() {
+      for (void* x : q) cudaFreeAsync(x, p->stream_);
+    }
+  } fr{this, {dh, dhf, v, u, part}};
+  check_cuda(cudaMemcpyAsync(dh, h64_.data(), K * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+  check_cuda(cudaMemcpyAsync(dhf, hf.data(), K * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+  check_cuda(launch_fill_f64(v, 1.0 / std::sqrt(static_cast<double>(nx)), nx, stream_), "fill");
+  st_[2].launches++;
+  for (size_t i = 0; i < power_iters; ++i) {
+    // u = A v_i with v_i = w_{i-1} / lambda_{i-1} folded in as an output scale
+    long long nb = 0;
+    check_cuda(launch_corr_f64(v, mz_, my_, mx_, u, oz, oy, ox, dhf, KZ_, KY_, KX_, -2 * pz_, -2 * py_,
+                               -2 * px_, i ? lam + i - 1 : nullptr, nullptr, &nb, stream_),
+               "corr_f64 launch");
+    // w = A^T u (valid correlation), ||w||^2 per block
+    check_cuda(launch_corr_f64(u, oz, oy, ox, v, mz_, my_, mx_, dh, KZ_, KY_, KX_, 0, 0, 0, nullptr, part,
+                               &nb, stream_),
+               "corr_f64 launch");
+    check_cuda(launch_finalize(part, nb, 1, kFinNorm, lam + i, nullptr, nullptr, nullptr, stream_),
+               "finalize launch");
+    st_[2].launches += 3;
+  }
+  check_cuda(cudaMemcpyAsync(hsc_, lam, power_iters * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  sync();
+  for (size_t i = 0; i < power_iters; ++i)
+    if (!(hsc_[i] > 0.0) || !std::isfinite(hsc_[i]))
+      fail(NDC_ERR_NUMERIC, "estimate_step: degenerate convolution operator");
   return 1.0 / hsc_[power_iters - 1];
 }
 

@@ -88,6 +88,7 @@ class Plan {
   void op_normal_gradient();           // g = A^T (A x - y)
   double op_kkt_residual();            // max|min(x, A^T(Ax - y))|
   double estimate_step(size_t power_iters);
+  double estimate_step_f64(size_t power_iters);  // small problems (reference-exact)
 
   // --- projected gradient (solvers.hpp:155-238) ---
   void pg_begin(const ndc_deconv_config& cfg);

@@ -83,24 +83,24 @@ def test_solver_kats(nd, golden_solvers):
 
 
 def test_random_family(nd, golden_solvers, oracle_c):
-    """test_solvers.cpp:95-112 family, 40 iterations, tol 0, with the reference's own
-    step (1/lambda from its f64 power iteration).  On these tiny shapes all-ones is
-    often an exact eigenvector of A^T A that is not the dominant one (e.g. x (2,1) with
-    a (5,1) kernel: A^T A is 2x2 symmetric Toeplitz); the f64 reference stays in that
-    eigenspace for all 30 power iterations while float32 rounding seeds the dominant
-    direction, so the device's auto step is the true 1/lambda_max rather than the
-    reference's.  The auto-step path is held to the reference on config 1 below and on
-    the estimate_step KATs (test_gpu_ops.py)."""
+    """test_solvers.cpp:95-112 family, 40 iterations, tol 0, auto step.  On these tiny
+    shapes all-ones is often an exact eigenvector of A^T A that is not the dominant one
+    (e.g. x (2,1) with a (5,1) kernel: A^T A is 2x2 symmetric Toeplitz); the f64
+    reference stays in that eigenspace for all 30 power iterations, and so does the
+    device, whose power iteration runs in float64 for small problems -- the step must
+    match the reference's to ~1e-12."""
     d = golden_solvers
     n = int(d["npg"])
     for i in range(n - 5):
         xs = tuple(int(v) for v in d[f"pg_xs{i}"])
+        s_ref = oracle_c.estimate_step(d[f"pg_h{i}"], xs, 30)
+        assert abs(nd.estimate_step(d[f"pg_h{i}"], xs, 30) - s_ref) <= 1e-12 * s_ref, i
         # The reference's own test asserts strict decrease, nonnegativity and trace
         # lengths (test_solvers.cpp:95-112); these random kernels (taps in [-1, 1]) are
         # ill-conditioned enough that float32 and f64 runs whose backtracking decisions
         # part ways settle up to ~1e-4 apart on a flat optimum, so the estimate is held
         # to 1e-3 here (the well-conditioned PSF cases below hold 1e-4).
-        _check(nd, d, i, tol=1e-3, step=oracle_c.estimate_step(d[f"pg_h{i}"], xs, 30))
+        _check(nd, d, i, tol=1e-3)
 
 
 def test_acceptance6_backtracking(nd, golden_solvers):
