@@ -44,7 +44,8 @@ typedef enum ndc_status {
   NDC_ERR_CUDA = 6,
   NDC_ERR_NCCL = 7,
   NDC_ERR_NO_DEVICE = 8,
-  NDC_ERR_ARGUMENT = 9     /* null pointer / capacity too small                    */
+  NDC_ERR_ARGUMENT = 9,    /* null pointer / capacity too small                    */
+  NDC_ERR_FORMAT = 10      /* ndconv::FormatError  (imageio.hpp: bad / truncated files) */
 } ndc_status;
 
 /* solvers.hpp:37-46 */
@@ -157,6 +158,19 @@ ndc_status ndc_deconv_rl_f64(int ndim, const size_t* y_ext, const double* y, con
                              double* x_out, double* obj_trace, double* kkt_trace, size_t trace_cap,
                              ndc_deconv_report* report);
 
+/* ---- tensor files (imageio.hpp) ----
+ * NDTENSOR: "NDTENSOR <ndim> <d_1> ... <d_n>\n" + little-endian f64 payload
+ * (imageio.hpp:24-125).  info: header only (ndim <= 16; extents into ext[16]). */
+ndc_status ndc_ndtensor_info(const char* path, int* ndim, size_t* ext16);
+ndc_status ndc_ndtensor_read_f64(const char* path, double* out, size_t capacity);
+ndc_status ndc_ndtensor_write_f64(const char* path, int ndim, const size_t* ext, const double* data);
+/* PGM P5/P2 (imageio.hpp:126-265): samples as doubles, shape (height, width); writes
+ * 8-bit P5 with round-half-even, clamping to [0,255] when clamp != 0. */
+ndc_status ndc_pgm_info(const char* path, size_t* height, size_t* width);
+ndc_status ndc_pgm_read_f64(const char* path, double* out, size_t capacity);
+ndc_status ndc_pgm_write_f64(const char* path, size_t height, size_t width, const double* data,
+                             int clamp);
+
 /* ---- device-resident plan (same operators, buffers kept in HBM between calls) ----
  * A plan owns the device buffers for `batch` images of one (x_ext, k_ext) problem, a
  * CUDA stream, and -- for z-slab sharded runs -- an NCCL communicator.  All calls on
@@ -181,6 +195,12 @@ ndc_status ndc_plan_get_report(ndc_plan* plan, size_t image, ndc_deconv_report* 
                                double* obj_trace, double* kkt_trace, size_t trace_cap);
 ndc_status ndc_plan_get_estimate_f64(ndc_plan* plan, double* x_out);
 ndc_status ndc_plan_get_estimate_f32(ndc_plan* plan, float* x_out);
+/* Stream an NDTENSOR observation file straight into the plan (pinned 16 MB chunks, no
+ * full host copy; a batch plan reads [batch, y_ext...] or, for batch 1, [y_ext...];
+ * a sharded plan reads only its own planes), and stream the estimate back out
+ * (sharded ranks each write their planes into one file; rank 0 writes the header). */
+ndc_status ndc_plan_load_observation_ndtensor(ndc_plan* plan, const char* path);
+ndc_status ndc_plan_save_estimate_ndtensor(ndc_plan* plan, const char* path);
 /* One forward (A x) / adjoint (A^T y) pass on resident buffers, for kernel timing. */
 ndc_status ndc_plan_forward(ndc_plan* plan);
 ndc_status ndc_plan_adjoint(ndc_plan* plan);

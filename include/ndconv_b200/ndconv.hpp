@@ -60,6 +60,7 @@ inline void check(ndc_status s) {
     case NDC_ERR_SHAPE: throw ShapeError(msg);
     case NDC_ERR_NUMERIC: throw NumericError(msg);
     case NDC_ERR_BOUNDS: throw BoundsError(msg);
+    case NDC_ERR_FORMAT: throw FormatError(msg);
     case NDC_ERR_ARGUMENT: throw std::invalid_argument(msg);
     default: throw DeviceError(msg);
   }
@@ -477,5 +478,56 @@ inline DeconvReport deconv_rl(const Tensor& y, const Kernel& h, const Shape& x_s
                                 &r));
   return b200::report_of(x_shape, std::move(x), r, obj.data(), kkt.data());
 }
+
+// ---- tensor files (imageio.hpp) ----------------------------------------------------------
+namespace io {
+
+inline Tensor read_tensor(const std::string& path) {
+  int nd = 0;
+  std::size_t ext[16];
+  b200::check(ndc_ndtensor_info(path.c_str(), &nd, ext));
+  Shape s(std::vector<std::size_t>(ext, ext + nd));
+  std::vector<double> v(s.element_count());
+  b200::check(ndc_ndtensor_read_f64(path.c_str(), v.data(), v.size()));
+  return Tensor(std::move(s), std::move(v));
+}
+
+inline void write_tensor(const Tensor& t, const std::string& path) {
+  b200::check(ndc_ndtensor_write_f64(path.c_str(), static_cast<int>(t.shape().ndim()),
+                                     t.shape().extents().data(), t.data().data()));
+}
+
+inline Tensor read_pgm(const std::string& path) {
+  std::size_t h = 0, w = 0;
+  b200::check(ndc_pgm_info(path.c_str(), &h, &w));
+  std::vector<double> v(h * w);
+  b200::check(ndc_pgm_read_f64(path.c_str(), v.data(), v.size()));
+  return Tensor(Shape{h, w}, std::move(v));
+}
+
+inline void write_pgm(const Tensor& t, const std::string& path, bool clamp) {
+  if (t.shape().ndim() != 2)
+    throw ShapeError("write_pgm: need a 2-d tensor, got " + t.shape().to_string());
+  b200::check(ndc_pgm_write_f64(path.c_str(), t.shape().extent(0), t.shape().extent(1),
+                                t.data().data(), clamp ? 1 : 0));
+}
+
+}  // namespace io
+
+// ---- metrics (simulation.hpp:195-208) ------------------------------------------------------
+namespace sim {
+inline double snr_db(const Tensor& reference, const Tensor& estimate) {
+  ndconv::detail::check_same_shape(reference, estimate, "snr_db");
+  double ref = 0.0, err = 0.0;
+  for (std::size_t i = 0; i < reference.size(); ++i) {
+    ref += reference[i] * reference[i];
+    const double e = estimate[i] - reference[i];
+    err += e * e;
+  }
+  if (ref == 0.0) throw NumericError("snr_db: reference is all zero, metric undefined");
+  if (err == 0.0) return std::numeric_limits<double>::infinity();
+  return 10.0 * std::log10(ref / err);
+}
+}  // namespace sim
 
 }  // namespace ndconv

@@ -25,7 +25,7 @@ LIBS = {
 }
 PREFIX = {"c": "oc_", "ref": "ref_"}
 
-RC_NAMES = {1: "Error", 2: "ShapeError", 3: "NumericError", 4: "BoundsError", 9: "Other"}
+RC_NAMES = {1: "Error", 2: "ShapeError", 3: "NumericError", 4: "BoundsError", 5: "FormatError", 9: "Other"}
 STOP_NAMES = {0: "converged", 1: "max_iters", 2: "stalled"}
 
 
@@ -208,3 +208,50 @@ class Oracle:
                    C.c_size_t(max_backtracks), C.c_size_t(iters), _ptr(x), _ptr(ax), _ptr(_f64(aty)),
                    C.byref(fo), C.byref(acc))
         return fo.value, acc.value
+
+    # --- tensor file formats (reference only: ref_shim.cpp ref_io_*) -------------------
+    def _ref_only(self, what):
+        if self.kind != "ref":
+            raise NotImplementedError(f"{what} is a reference-shim entry point")
+
+    def _parse(self, name, data: bytes) -> np.ndarray:
+        self._ref_only(name)
+        nd = C.c_int()
+        ext = (C.c_size_t * 16)()
+        self._call(name, data, C.c_size_t(len(data)), C.byref(nd), ext, None, C.c_size_t(0))
+        out = np.empty(tuple(int(ext[i]) for i in range(nd.value)), np.float64)
+        self._call(name, data, C.c_size_t(len(data)), C.byref(nd), ext, _ptr(out), C.c_size_t(out.size))
+        return out
+
+    def parse_tensor(self, data: bytes) -> np.ndarray:
+        """imageio.hpp:78-120 read_tensor(std::istream&) on ``data``."""
+        return self._parse("io_parse_tensor", data)
+
+    def parse_pgm(self, data: bytes) -> np.ndarray:
+        """imageio.hpp:184-231 read_pgm(std::istream&) on ``data``."""
+        return self._parse("io_parse_pgm", data)
+
+    def _serialize(self, name, t, *extra) -> bytes:
+        self._ref_only(name)
+        t = _f64(t)
+        n = C.c_size_t()
+        self._call(name, C.c_int(t.ndim), _ext(t.shape), _ptr(t), *extra, None, C.c_size_t(0), C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        self._call(name, C.c_int(t.ndim), _ext(t.shape), _ptr(t), *extra, buf, C.c_size_t(n.value), C.byref(n))
+        return buf.raw[: n.value]
+
+    def serialize_tensor(self, t) -> bytes:
+        """imageio.hpp:63-71 write_tensor(t, std::ostream&)."""
+        return self._serialize("io_serialize_tensor", t)
+
+    def serialize_pgm(self, t, clamp: bool = False) -> bytes:
+        """imageio.hpp:238-260 write_pgm(t, std::ostream&, clamp)."""
+        return self._serialize("io_serialize_pgm", t, C.c_int(1 if clamp else 0))
+
+    def snr_db(self, a, b) -> float:
+        """simulation.hpp:195-208."""
+        self._ref_only("snr_db")
+        a, b = _f64(a), _f64(b)
+        out = C.c_double()
+        self._call("snr_db", C.c_int(a.ndim), _ext(a.shape), _ptr(a), _ptr(b), C.byref(out))
+        return out.value

@@ -13,6 +13,8 @@
 #include <cstddef>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "ndconv/ndconv.hpp"
@@ -21,7 +23,7 @@
 
 namespace {
 
-enum { RC_OK = 0, RC_ERROR = 1, RC_SHAPE = 2, RC_NUMERIC = 3, RC_BOUNDS = 4, RC_OTHER = 9 };
+enum { RC_OK = 0, RC_ERROR = 1, RC_SHAPE = 2, RC_NUMERIC = 3, RC_BOUNDS = 4, RC_FORMAT = 5, RC_OTHER = 9 };
 
 struct PgCfg {  // layout shared with oc_pg_config / ndc_deconv_config
   std::size_t max_iters;
@@ -62,6 +64,8 @@ int guard(F&& f) {
     return RC_NUMERIC;
   } catch (const ndconv::BoundsError&) {
     return RC_BOUNDS;
+  } catch (const ndconv::FormatError&) {
+    return RC_FORMAT;
   } catch (const ndconv::Error&) {
     return RC_ERROR;
   } catch (...) {
@@ -285,4 +289,59 @@ REF_API int ref_pg_iterations(int ndim, const std::size_t* yext, const double* y
     *f_io = f;
     *accepted_out = accepted_total;
   });
+}
+
+// ---- tensor file formats (imageio.hpp), over in-memory byte strings ---------------------
+// Parsing and serialising through the reference's own istream/ostream entry points pins
+// the B200 library's NDTENSOR / PGM readers and writers byte for byte (tests/test_io.py).
+namespace {
+int emit(const std::string& s, char* out, std::size_t cap, std::size_t* n) {
+  *n = s.size();
+  if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+  return RC_OK;
+}
+
+void take(const ndconv::Tensor& t, int* ndim, std::size_t* ext, double* out, std::size_t cap) {
+  *ndim = static_cast<int>(t.shape().ndim());
+  for (std::size_t i = 0; i < t.shape().ndim() && i < 16; ++i) ext[i] = t.shape().extent(i);
+  if (out && cap >= t.size()) put(t, out);
+}
+}  // namespace
+
+REF_API int ref_io_parse_tensor(const char* bytes, std::size_t nbytes, int* ndim, std::size_t* ext,
+                                double* out, std::size_t cap) {
+  return guard([&] {
+    std::istringstream in(std::string(bytes, nbytes), std::ios::binary);
+    take(ndconv::io::read_tensor(in), ndim, ext, out, cap);
+  });
+}
+
+REF_API int ref_io_serialize_tensor(int ndim, const std::size_t* ext, const double* v, char* out,
+                                    std::size_t cap, std::size_t* n) {
+  return guard([&] {
+    std::ostringstream os(std::ios::binary);
+    ndconv::io::write_tensor(tensor_of(ndim, ext, v), os);
+    emit(os.str(), out, cap, n);
+  });
+}
+
+REF_API int ref_io_parse_pgm(const char* bytes, std::size_t nbytes, int* ndim, std::size_t* ext,
+                             double* out, std::size_t cap) {
+  return guard([&] {
+    std::istringstream in(std::string(bytes, nbytes), std::ios::binary);
+    take(ndconv::io::read_pgm(in), ndim, ext, out, cap);
+  });
+}
+
+REF_API int ref_io_serialize_pgm(int ndim, const std::size_t* ext, const double* v, int clamp,
+                                 char* out, std::size_t cap, std::size_t* n) {
+  return guard([&] {
+    std::ostringstream os(std::ios::binary);
+    ndconv::io::write_pgm(tensor_of(ndim, ext, v), os, clamp != 0);
+    emit(os.str(), out, cap, n);
+  });
+}
+
+REF_API int ref_snr_db(int ndim, const std::size_t* ext, const double* a, const double* b, double* out) {
+  return guard([&] { *out = ndconv::sim::snr_db(tensor_of(ndim, ext, a), tensor_of(ndim, ext, b)); });
 }

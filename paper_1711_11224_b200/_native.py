@@ -91,6 +91,14 @@ _SIGS = [
                                       C.c_size_t]),
     ("ndc_plan_get_estimate_f64", C.c_int, [C.c_void_p, dbl_p]),
     ("ndc_plan_get_estimate_f32", C.c_int, [C.c_void_p, flt_p]),
+    ("ndc_plan_load_observation_ndtensor", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("ndc_plan_save_estimate_ndtensor", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("ndc_ndtensor_info", C.c_int, [C.c_char_p, C.POINTER(C.c_int), size_t_p]),
+    ("ndc_ndtensor_read_f64", C.c_int, [C.c_char_p, dbl_p, C.c_size_t]),
+    ("ndc_ndtensor_write_f64", C.c_int, [C.c_char_p, C.c_int, size_t_p, dbl_p]),
+    ("ndc_pgm_info", C.c_int, [C.c_char_p, size_t_p, size_t_p]),
+    ("ndc_pgm_read_f64", C.c_int, [C.c_char_p, dbl_p, C.c_size_t]),
+    ("ndc_pgm_write_f64", C.c_int, [C.c_char_p, C.c_size_t, C.c_size_t, dbl_p, C.c_int]),
     ("ndc_plan_forward", C.c_int, [C.c_void_p]),
     ("ndc_plan_adjoint", C.c_int, [C.c_void_p]),
     ("ndc_plan_set_timing", C.c_int, [C.c_void_p, C.c_int]),

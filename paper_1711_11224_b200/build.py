@@ -17,10 +17,12 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libndconv_b200.so")
+CLI = os.path.join(PKG, "ndconv")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
 SOURCES = ["ndc_corr_sh0_ry1.cu", "ndc_corr_sh0_ry2.cu", "ndc_corr_sh2_ry1.cu", "ndc_corr_sh2_ry2.cu",
-           "ndc_kernels.cu", "ndc_plan.cu", "ndc_capi.cu", "ndc_comm.cu"]
-HEADERS = ["ndc_internal.h", "ndc_plan.h", "ndc_correlate.cuh", os.path.join("..", "..", "include", "ndconv_b200.h")]
+           "ndc_kernels.cu", "ndc_plan.cu", "ndc_capi.cu", "ndc_comm.cu", "ndc_io.cu"]
+HEADERS = ["ndc_internal.h", "ndc_plan.h", "ndc_correlate.cuh", "ndc_io.h", os.path.join("..", "..", "include", "ndconv_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                 "-Xptxas", "-v", "-I", os.path.join(PKG, "..", "include")]
@@ -63,7 +65,22 @@ def build(verbose: bool = False) -> str:
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}{p.stderr}")
+    build_cli()
     return LIB
+
+
+def build_cli() -> str:
+    """The `ndconv` command-line drop-in (tools/main.cpp), linked against the library."""
+    src = os.path.join(CSRC, "ndconv_cli.cpp")
+    inc = os.path.join(PKG, "..", "include")
+    deps = [src, LIB, os.path.join(inc, "ndconv_b200.h"), os.path.join(inc, "ndconv_b200", "ndconv.hpp")]
+    if _newer(CLI, deps):
+        cmd = [CXX, "-std=c++20", "-O2", "-Wall", "-I", inc, src, "-o", CLI, f"-L{PKG}", "-l:libndconv_b200.so",
+               "-Wl,-rpath,$ORIGIN"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"ndconv CLI build failed:\n{p.stdout}{p.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "ndc_io.h"
 #include "ndc_plan.h"
 
 struct ndc_plan {
@@ -381,6 +382,77 @@ ndc_status ndc_plan_get_estimate_f64(ndc_plan* plan, double* x_out) {
 ndc_status ndc_plan_get_estimate_f32(ndc_plan* plan, float* x_out) {
   NDC_PLAN(need(x_out, "x_out"); plan->p->get_estimate_f32(x_out));
 }
+ndc_status ndc_plan_load_observation_ndtensor(ndc_plan* plan, const char* path) {
+  NDC_PLAN(need(path, "path"); plan->p->load_observation_ndtensor(path));
+}
+ndc_status ndc_plan_save_estimate_ndtensor(ndc_plan* plan, const char* path) {
+  NDC_PLAN(need(path, "path"); plan->p->save_estimate_ndtensor(path));
+}
+
+// ---- tensor files ---------------------------------------------------------------------------
+ndc_status ndc_ndtensor_info(const char* path, int* ndim, size_t* ext16) {
+  return guard([&] {
+    need(path, "path");
+    need(ndim, "ndim");
+    need(ext16, "ext");
+    const ndc::NdtHeader h = ndc::read_ndtensor_header(path);
+    *ndim = static_cast<int>(h.ext.size());
+    for (size_t i = 0; i < h.ext.size(); ++i) ext16[i] = h.ext[i];
+  });
+}
+
+ndc_status ndc_ndtensor_read_f64(const char* path, double* out, size_t capacity) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    ndc::read_ndtensor(path, out, capacity, nullptr);
+  });
+}
+
+ndc_status ndc_ndtensor_write_f64(const char* path, int ndim, const size_t* ext, const double* data) {
+  return guard([&] {
+    need(path, "path");
+    need(ext, "ext");
+    need(data, "data");
+    check_ndim(ndim);
+    for (int i = 0; i < ndim; ++i)
+      if (ext[i] == 0) ndc::fail(NDC_ERR_SHAPE, "Shape: extents must be positive");
+    ndc::write_ndtensor(path, std::vector<size_t>(ext, ext + ndim), data);
+  });
+}
+
+ndc_status ndc_pgm_info(const char* path, size_t* height, size_t* width) {
+  return guard([&] {
+    need(path, "path");
+    need(height, "height");
+    need(width, "width");
+    std::vector<double> d;
+    ndc::read_pgm(path, &d, height, width);
+  });
+}
+
+ndc_status ndc_pgm_read_f64(const char* path, double* out, size_t capacity) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    std::vector<double> d;
+    size_t h = 0, w = 0;
+    ndc::read_pgm(path, &d, &h, &w);
+    if (capacity < d.size()) ndc::fail(NDC_ERR_ARGUMENT, "read_pgm: output capacity too small");
+    std::memcpy(out, d.data(), d.size() * 8);
+  });
+}
+
+ndc_status ndc_pgm_write_f64(const char* path, size_t height, size_t width, const double* data,
+                             int clamp) {
+  return guard([&] {
+    need(path, "path");
+    need(data, "data");
+    if (height == 0 || width == 0) ndc::fail(NDC_ERR_SHAPE, "Shape: extents must be positive");
+    ndc::write_pgm(path, height, width, data, clamp != 0);
+  });
+}
+
 ndc_status ndc_plan_forward(ndc_plan* plan) { NDC_PLAN(plan->p->bench_forward()); }
 ndc_status ndc_plan_adjoint(ndc_plan* plan) { NDC_PLAN(plan->p->bench_adjoint()); }
 ndc_status ndc_plan_set_timing(ndc_plan* plan, int enabled) {

@@ -11,6 +11,9 @@
 #include <mutex>
 #include <thread>
 
+#include <cstdio>
+
+#include "ndc_io.h"
 #include "ndc_plan.h"
 
 namespace ndc {
@@ -742,6 +745,138 @@ double Plan::estimate_step(size_t power_iters) {
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   sync();
   return 1.0 / hsc_[power_iters - 1];
+}
+
+// ---- NDTENSOR streaming (imageio.hpp:24-125 format) ----------------------------------------
+namespace {
+// First non-finite index in v[0, n) (n when none), checked by several threads.
+size_t first_nonfinite(const double* v, size_t n) {
+  const unsigned t = std::max(1u, std::min(8u, static_cast<unsigned>(n >> 18)));
+  std::vector<size_t> bad(t, n);
+  std::vector<std::thread> th;
+  const size_t per = (n + t - 1) / t;
+  for (unsigned i = 0; i < t; ++i)
+    th.emplace_back([&, i] {
+      const size_t lo = i * per, hi = std::min(n, lo + per);
+      for (size_t k = lo; k < hi; ++k)
+        if (!std::isfinite(v[k])) {
+          bad[i] = k;
+          return;
+        }
+    });
+  for (auto& x : th) x.join();
+  return *std::min_element(bad.begin(), bad.end());
+}
+
+struct FileCloser {
+  std::FILE* f;
+  ~FileCloser() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+std::vector<size_t> Plan::user_shape(bool y) const {
+  std::vector<size_t> e;
+  if (B_ > 1) e.push_back(B_);
+  const int lead = 3 - ndim_;
+  for (int i = 0; i < ndim_; ++i) {
+    const size_t k = kext_[lead + i];
+    e.push_back(y ? xext_[lead + i] + k - 1 : xext_[lead + i]);
+  }
+  return e;
+}
+
+void Plan::load_observation_ndtensor(const std::string& path) {
+  const NdtHeader h = read_ndtensor_header(path);
+  if (h.ext != user_shape(true))
+    fail(NDC_ERR_SHAPE, "load_observation: file shape does not match the plan's observation shape");
+  ensure_pinned();
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path);
+  FileCloser fc{f};
+  const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;                       // dense
+  const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;               // one image
+  const size_t own = static_cast<size_t>(yb_ - ya_) * plane;
+  const size_t chunk = (size_t(16) << 20) / 8;
+  size_t i = 0;
+  for (size_t b = 0; b < B_; ++b) {
+    const size_t first = b * full + static_cast<size_t>(ya_) * plane;
+    if (std::fseek(f, static_cast<long>(h.payload_offset + first * 8), SEEK_SET) != 0)
+      fail(NDC_ERR_FORMAT, "read_tensor: seek failure");
+    for (size_t off = 0; off < own; off += chunk, ++i) {
+      const int s = static_cast<int>(i & 1);
+      const size_t n = std::min(chunk, own - off);
+      if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+      double* buf = static_cast<double*>(hpin_[s]);
+      if (std::fread(buf, 8, n, f) != n)
+        fail(NDC_ERR_FORMAT, "read_tensor: truncated payload at element " + std::to_string(first + off));
+      const size_t bad = first_nonfinite(buf, n);
+      if (bad < n)
+        fail(NDC_ERR_FORMAT, "read_tensor: non-finite value at element " + std::to_string(first + off + bad));
+      check_cuda(cudaMemcpyAsync(static_cast<double*>(staging_) + off, buf, n * 8, cudaMemcpyHostToDevice,
+                                 stream_),
+                 "H2D");
+      check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
+    }
+    check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
+                               yobs_ + b * Y_.image + static_cast<long long>(ya_ - rlo_) * Y_.plane, 1,
+                               Y_.geo(yb_ - ya_), stream_),
+               "pack");
+    st_[2].launches++;
+  }
+  sync();
+  halo_y(yobs_);
+}
+
+void Plan::save_estimate_ndtensor(const std::string& path) {
+  const std::vector<size_t> ext = user_shape(false);
+  const std::string hl = ndtensor_header_line(ext);
+  const size_t plane = static_cast<size_t>(my_) * mx_;
+  const size_t full = static_cast<size_t>(mz_) * plane;
+  if (rank_ == 0) {  // header + full-size file, then every rank fills its planes
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
+    FileCloser fc{f};
+    bool ok = std::fwrite(hl.data(), 1, hl.size(), f) == hl.size();
+    ok = ok && std::fseek(f, static_cast<long>(hl.size() + full * B_ * 8 - 1), SEEK_SET) == 0;
+    ok = ok && std::fputc(0, f) != EOF;
+    if (!ok) fail(NDC_ERR_FORMAT, "write_tensor: stream failure");
+  }
+  if (world_ > 1) {  // barrier: the file exists before the other ranks open it
+    comm_->allgather(dsc_, gather_, 1, stream_);
+    sync();
+  }
+  ensure_pinned();
+  std::FILE* f = std::fopen(path.c_str(), "r+b");
+  if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
+  FileCloser fc{f};
+  const size_t own = static_cast<size_t>(xa_n_) * plane;
+  const size_t chunk = (size_t(16) << 20) / 8;
+  for (size_t b = 0; b < B_; ++b) {
+    check_cuda(launch_unpack_f64(x_owned(x_) + b * X_.image, static_cast<double*>(staging_), 1,
+                                 X_.geo(xa_n_), stream_),
+               "unpack");
+    st_[2].launches++;
+    const size_t first = b * full + static_cast<size_t>(xa_) * plane;
+    if (std::fseek(f, static_cast<long>(hl.size() + first * 8), SEEK_SET) != 0)
+      fail(NDC_ERR_FORMAT, "write_tensor: seek failure");
+    for (size_t off = 0; off < own; off += chunk) {
+      const size_t n = std::min(chunk, own - off);
+      double* buf = static_cast<double*>(hpin_[0]);
+      check_cuda(cudaMemcpyAsync(buf, static_cast<const double*>(staging_) + off, n * 8,
+                                 cudaMemcpyDeviceToHost, stream_),
+                 "D2H");
+      sync();
+      if (first_nonfinite(buf, n) < n)
+        fail(NDC_ERR_NUMERIC, "write_tensor: refusing to store non-finite values");
+      if (std::fwrite(buf, 8, n, f) != n) fail(NDC_ERR_FORMAT, "write_tensor: stream failure");
+    }
+  }
+  if (world_ > 1) {  // every rank's planes are on disk before any returns
+    comm_->allgather(dsc_, gather_, 1, stream_);
+    sync();
+  }
 }
 
 // solvers.hpp:127-143 in float64 on dense scratch buffers (small problems only).

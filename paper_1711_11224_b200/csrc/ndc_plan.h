@@ -80,6 +80,9 @@ class Plan {
   void get_estimate_f32(float* x);
   void get_y_buffer_f64(double* y);              // the y-shaped result buffer (A x)
   void get_x_buffer_f64(double* x, int which);   // 0 = x, 1 = g
+  void load_observation_ndtensor(const std::string& path);  // streamed, owned planes
+  void save_estimate_ndtensor(const std::string& path);
+  std::vector<size_t> user_shape(bool y) const;   // [batch,] extents as the caller sees them
 
   // --- operators on resident buffers (the one-shot C-ABI entry points use these) ---
   void op_conv_full();                 // r = A x            (store)

@@ -47,7 +47,7 @@ class DeviceError(Error):
 
 
 _RC = {1: Error, 2: ShapeError, 3: NumericError, 4: BoundsError, 5: UnsupportedError,
-       6: DeviceError, 7: DeviceError, 8: DeviceError, 9: ValueError}
+       6: DeviceError, 7: DeviceError, 8: DeviceError, 9: ValueError, 10: FormatError}
 
 
 def _check(rc: int):
@@ -285,6 +285,47 @@ def deconv_rl(y, h, x_shape, cfg: RlConfig | None = None) -> DeconvReport:
     return _report(x, rep, obj, kkt)
 
 
+# --- tensor files (imageio.hpp) -------------------------------------------------------------
+
+
+def _path(p) -> bytes:
+    return str(p).encode()
+
+
+def read_tensor(path) -> np.ndarray:
+    """imageio.hpp:84-125 NDTENSOR reader (strict header / payload validation)."""
+    nd_ = C.c_int()
+    ext = (C.c_size_t * 16)()
+    _check(N.lib().ndc_ndtensor_info(_path(path), C.byref(nd_), ext))
+    shape = tuple(int(ext[i]) for i in range(nd_.value))
+    out = np.empty(shape, np.float64)
+    _check(N.lib().ndc_ndtensor_read_f64(_path(path), _p(out), out.size))
+    return out
+
+
+def write_tensor(t, path) -> None:
+    """imageio.hpp:63-81 NDTENSOR writer (refuses non-finite values)."""
+    t = _f64(t)
+    _check(N.lib().ndc_ndtensor_write_f64(_path(path), t.ndim, _ext(t.shape), _p(t)))
+
+
+def read_pgm(path) -> np.ndarray:
+    """imageio.hpp:186-238: P5/P2 samples as doubles, shape (height, width)."""
+    h, w = C.c_size_t(), C.c_size_t()
+    _check(N.lib().ndc_pgm_info(_path(path), C.byref(h), C.byref(w)))
+    out = np.empty((h.value, w.value), np.float64)
+    _check(N.lib().ndc_pgm_read_f64(_path(path), _p(out), out.size))
+    return out
+
+
+def write_pgm(t, path, clamp: bool = True) -> None:
+    """imageio.hpp:240-265: 8-bit P5, round half to even, optional clamp."""
+    t = _f64(t)
+    if t.ndim != 2:
+        raise ShapeError(f"write_pgm: need a 2-d tensor, got {t.shape}")
+    _check(N.lib().ndc_pgm_write_f64(_path(path), t.shape[0], t.shape[1], _p(t), 1 if clamp else 0))
+
+
 # --- device-resident plan ----------------------------------------------------------------
 
 
@@ -379,6 +420,13 @@ class Plan:
         else:
             y = _f64(y)
             _check(N.lib().ndc_plan_set_observation_f64(self.handle, _p(y)))
+
+    def load_observation(self, path):
+        """Stream an NDTENSOR observation file into the plan (owned planes only)."""
+        _check(N.lib().ndc_plan_load_observation_ndtensor(self.handle, _path(path)))
+
+    def save_estimate(self, path):
+        _check(N.lib().ndc_plan_save_estimate_ndtensor(self.handle, _path(path)))
 
     def pg_begin(self, cfg: DeconvConfig | None = None):
         c = (cfg or DeconvConfig()).to_c()

@@ -1,0 +1,222 @@
+"""`ndconv` command-line drop-in (reference tools/main.cpp), restating
+tests/test_cli.cpp.  Usage / format / shape paths and `metrics` are host-only and run
+on CPU; `convolve` and `deconv` run the device path and are marked gpu.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1711_11224_b200 import build as B
+from paper_1711_11224_b200 import ndconv as nd
+
+# main.cpp:161-179: the deconv manifest's keys, in order (trace_csv / final_kkt /
+# negative_pixels_clamped are conditional).
+DECONV_KEYS = ["subcommand", "version", "observed", "kernel", "output", "method", "shape", "max_iters", "tol",
+               "step", "seedless", "trace_csv", "stop_reason", "iterations_run", "final_objective", "final_kkt",
+               "negative_pixels_clamped", "wall_time_seconds"]
+
+
+@pytest.fixture(scope="module")
+def cli():
+    if not os.path.exists(B.CLI):
+        B.build()
+    return B.CLI
+
+
+def run(cli, args, cwd):
+    p = subprocess.run([cli, *args], cwd=cwd, capture_output=True, text=True, timeout=300)
+    return p.returncode, p.stdout, p.stderr
+
+
+def manifest(path):
+    out = {}
+    order = []
+    for line in open(path):
+        k, v = line.rstrip("\n").split("=", 1)
+        out[k] = v
+        order.append(k)
+    return out, order
+
+
+# --- CPU ---------------------------------------------------------------------------------
+def test_usage_errors_exit_2_and_help_0(cli, tmp_path):
+    assert run(cli, [], tmp_path)[0] == 2
+    assert run(cli, ["--help"], tmp_path)[0] == 0
+    assert run(cli, ["convolve", "--no-such-flag"], tmp_path)[0] == 2
+    assert run(cli, ["deconv", "--observed", "a", "--kernel", "b", "--shape", "4", "--method", "bogus",
+                     "--output", "c"], tmp_path)[0] == 2
+    assert run(cli, ["deconv", "--observed", "a", "--kernel", "b", "--shape", "4,0", "--output", "c"],
+               tmp_path)[0] == 2
+    assert run(cli, ["deconv", "--observed", "a", "--kernel", "b", "--shape", "4", "--tol", "-1",
+                     "--output", "c"], tmp_path)[0] == 2
+    assert run(cli, ["--threads", "0", "metrics", "--reference", "a", "--estimate", "b"], tmp_path)[0] == 2
+    assert run(cli, ["frobnicate"], tmp_path)[0] == 2
+    assert run(cli, ["convolve", "--input"], tmp_path)[0] == 2
+
+
+def test_convolve_rejects_even_kernels_with_shape_code(cli, tmp_path):
+    nd.write_tensor(np.ones(2), str(tmp_path / "even.ndt"))
+    nd.write_tensor(np.arange(1.0, 5.0), str(tmp_path / "x.ndt"))
+    rc, _, _ = run(cli, ["convolve", "--input", "x.ndt", "--kernel", "even.ndt", "--output", "y.ndt"], tmp_path)
+    assert rc == 4
+
+
+def test_missing_input_files_exit_with_format_code(cli, tmp_path):
+    rc, _, _ = run(cli, ["convolve", "--input", "/nonexistent.ndt", "--kernel", "/nope.ndt", "--output",
+                         "y.ndt"], tmp_path)
+    assert rc == 3
+
+
+def test_deconv_shape_mismatch_exits_with_shape_code(cli, tmp_path):
+    nd.write_tensor(np.zeros((10, 10)), str(tmp_path / "obs.ndt"))
+    delta = np.zeros((3, 3))
+    delta[1, 1] = 1
+    nd.write_tensor(delta, str(tmp_path / "psf.ndt"))
+    rc, _, _ = run(cli, ["deconv", "--observed", "obs.ndt", "--kernel", "psf.ndt", "--shape", "9,9", "--output",
+                         "e.ndt"], tmp_path)
+    assert rc == 4
+
+
+def test_metrics_prints_decibels_or_inf(cli, tmp_path):
+    nd.write_tensor(np.array([3.0, 4.0]), str(tmp_path / "ref.ndt"))
+    nd.write_tensor(np.array([3.0, 3.0]), str(tmp_path / "est.ndt"))
+    rc, out, _ = run(cli, ["metrics", "--reference", "ref.ndt", "--estimate", "est.ndt"], tmp_path)
+    assert rc == 0 and out.startswith("13.979400086720")
+    rc, out, _ = run(cli, ["metrics", "--reference", "ref.ndt", "--estimate", "ref.ndt"], tmp_path)
+    assert rc == 0 and out.startswith("inf")
+    nd.write_tensor(np.zeros(3), str(tmp_path / "bad.ndt"))
+    assert run(cli, ["metrics", "--reference", "ref.ndt", "--estimate", "bad.ndt"], tmp_path)[0] == 4
+    nd.write_tensor(np.zeros(2), str(tmp_path / "zero.ndt"))
+    assert run(cli, ["metrics", "--reference", "zero.ndt", "--estimate", "ref.ndt"], tmp_path)[0] == 5
+
+
+@pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")
+def test_metrics_matches_reference_snr(cli, tmp_path):
+    rng = np.random.default_rng(5)
+    a, b = rng.standard_normal((6, 7)), rng.standard_normal((6, 7))
+    nd.write_tensor(a, str(tmp_path / "a.ndt"))
+    nd.write_tensor(b, str(tmp_path / "b.ndt"))
+    rc, out, _ = run(cli, ["metrics", "--reference", "a.ndt", "--estimate", "b.ndt"], tmp_path)
+    assert rc == 0
+    assert out.strip() == f"{O.Oracle('ref').snr_db(a, b):.12f}"
+
+
+def test_pgm_inputs_are_dispatched_by_extension(cli, tmp_path):
+    nd.write_pgm(np.array([[3.0, 4.0]]), str(tmp_path / "r.pgm"))
+    nd.write_tensor(np.array([[3.0, 3.0]]), str(tmp_path / "e.ndt"))
+    rc, out, _ = run(cli, ["metrics", "--reference", "r.pgm", "--estimate", "e.ndt"], tmp_path)
+    assert rc == 0 and out.startswith("13.979400086720")
+
+
+# --- GPU ---------------------------------------------------------------------------------
+@pytest.mark.gpu
+def test_convolve_delta_kernel_reproduces_input(cli, tmp_path, nd):
+    x = np.array([[1.0, 2.0], [3.0, 4.0]])
+    delta = np.zeros((3, 3))
+    delta[1, 1] = 1
+    nd.write_tensor(x, str(tmp_path / "x.ndt"))
+    nd.write_tensor(delta, str(tmp_path / "delta.ndt"))
+    rc, _, err = run(cli, ["convolve", "--input", "x.ndt", "--kernel", "delta.ndt", "--output", "y.ndt"], tmp_path)
+    assert rc == 0, err
+    y = nd.read_tensor(str(tmp_path / "y.ndt"))
+    assert y.shape == (4, 4)
+    assert np.array_equal(y[1:3, 1:3], x)
+    m, order = manifest(tmp_path / "y.ndt.manifest")
+    assert order == ["subcommand", "version", "input", "kernel", "output", "input_shape", "kernel_shape",
+                     "output_shape"]
+    assert m["subcommand"] == "convolve" and m["version"] == "0.1.0"
+    assert (m["input_shape"], m["kernel_shape"], m["output_shape"]) == ("2,2", "3,3", "4,4")
+
+
+@pytest.mark.gpu
+def test_convolve_matches_oracle(cli, tmp_path, nd, oracle_c, rel_l2):
+    rng = np.random.default_rng(21)
+    x, h = rng.uniform(0, 1, (37, 50)), rng.uniform(0, 1, (5, 7))
+    nd.write_tensor(x, str(tmp_path / "x.ndt"))
+    nd.write_tensor(h, str(tmp_path / "h.ndt"))
+    rc, _, err = run(cli, ["convolve", "--input", "x.ndt", "--kernel", "h.ndt", "--output", "y.ndt"], tmp_path)
+    assert rc == 0, err
+    assert rel_l2(nd.read_tensor(str(tmp_path / "y.ndt")), oracle_c.conv_full(x, h)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_pgm_outputs_are_written_clamped(cli, tmp_path, nd):
+    nd.write_tensor(np.array([[0.0, 128.0], [300.0, -5.0]]), str(tmp_path / "x.ndt"))
+    nd.write_tensor(np.ones((1, 1)), str(tmp_path / "delta.ndt"))
+    rc, _, err = run(cli, ["convolve", "--input", "x.ndt", "--kernel", "delta.ndt", "--output", "y.pgm"], tmp_path)
+    assert rc == 0, err
+    assert np.array_equal(nd.read_pgm(str(tmp_path / "y.pgm")), np.array([[0, 128], [255, 0]], np.float64))
+
+
+def _gaussian_psf(n, sigma):
+    c = np.arange(n) - n // 2
+    g = np.exp(-(c[:, None] ** 2 + c[None, :] ** 2) / (2 * sigma * sigma))
+    return g / g.sum()
+
+
+@pytest.mark.gpu
+def test_deconv_drives_objective_down_with_consistent_trace(cli, tmp_path, nd, oracle_c):
+    truth = np.zeros((32, 32))
+    truth[6, 6], truth[6, 24], truth[20, 12], truth[26, 26] = 1.5, 0.8, 2.0, 1.0
+    psf = _gaussian_psf(5, 1.0)
+    nd.write_tensor(psf, str(tmp_path / "psf.ndt"))
+    nd.write_tensor(oracle_c.conv_full(truth, psf), str(tmp_path / "observed.ndt"))
+    rc, _, err = run(cli, ["deconv", "--observed", "observed.ndt", "--kernel", "psf.ndt", "--shape", "32,32",
+                           "--method", "pg", "--max-iters", "500", "--tol", "0", "--step", "8", "--seedless",
+                           "--trace-csv", "trace.csv", "--output", "est.ndt"], tmp_path)
+    assert rc == 0, err
+    m, order = manifest(tmp_path / "est.ndt.manifest")
+    assert order == [k for k in DECONV_KEYS if k != "negative_pixels_clamped"]
+    assert m["method"] == "pg" and m["stop_reason"] == "max_iters" and m["seedless"] == "true"
+    assert m["shape"] == "32,32" and m["max_iters"] == "500" and m["step"] == "8" and m["tol"] == "0"
+    rows = open(tmp_path / "trace.csv").read().splitlines()
+    assert rows[0] == "iter,objective,kkt"
+    assert len(rows) == int(m["iterations_run"]) + 1
+    f_first, f_last = float(rows[1].split(",")[1]), float(rows[-1].split(",")[1])
+    assert f_last < 1e-6 * f_first
+    assert float(m["final_objective"]) == f_last
+    assert [int(r.split(",")[0]) for r in rows[1:]] == list(range(1, len(rows)))
+    est = nd.read_tensor(str(tmp_path / "est.ndt"))
+    assert np.linalg.norm(est - truth) <= 1e-2 * np.linalg.norm(truth)
+
+
+@pytest.mark.gpu
+def test_deconv_rl_conserves_flux(cli, tmp_path, nd, oracle_c):
+    rng = np.random.default_rng(4)
+    truth = np.zeros((24, 24))
+    for _ in range(3):
+        r = rng.integers(2, 22)
+        truth[r, 2:22] = 1.0
+    psf = _gaussian_psf(5, 1.0)
+    obs = oracle_c.conv_full(truth, psf)
+    nd.write_tensor(obs, str(tmp_path / "observed.ndt"))
+    nd.write_tensor(psf, str(tmp_path / "psf.ndt"))
+    rc, _, err = run(cli, ["deconv", "--observed", "observed.ndt", "--kernel", "psf.ndt", "--shape", "24,24",
+                           "--method", "rl", "--max-iters", "40", "--tol", "0", "--output", "est.ndt"], tmp_path)
+    assert rc == 0, err
+    est = nd.read_tensor(str(tmp_path / "est.ndt"))
+    # fp32 device arithmetic: flux is conserved to float rounding (reference: 1e-8 in f64)
+    assert abs(est.sum() - obs.sum()) <= 1e-5 * abs(obs.sum())
+    m, order = manifest(tmp_path / "est.ndt.manifest")
+    assert m["negative_pixels_clamped"] == "0"
+    assert order == [k for k in DECONV_KEYS if k not in ("trace_csv",)]
+
+
+@pytest.mark.gpu
+def test_deconv_stalled_exits_numeric(cli, tmp_path, nd):
+    # A zero kernel: no trial decreases the objective, the line search stalls (exit 5),
+    # but the estimate and manifest are still written first (main.cpp:158-183).
+    y = np.ones((6, 6))
+    nd.write_tensor(y, str(tmp_path / "y.ndt"))
+    nd.write_tensor(np.zeros((3, 3)), str(tmp_path / "h.ndt"))
+    rc, _, _ = run(cli, ["deconv", "--observed", "y.ndt", "--kernel", "h.ndt", "--shape", "4,4", "--step", "1",
+                         "--output", "e.ndt"], tmp_path)
+    m, _ = manifest(tmp_path / "e.ndt.manifest")
+    assert rc in (0, 5)
+    if m["stop_reason"] == "stalled":
+        assert rc == 5
