@@ -171,6 +171,21 @@ ndc_status ndc_pgm_read_f64(const char* path, double* out, size_t capacity);
 ndc_status ndc_pgm_write_f64(const char* path, size_t height, size_t width, const double* data,
                              int clamp);
 
+/* ---- simulation generators (simulation.hpp:36-191) ----
+ * Image-sized work runs on the device (phantoms bit-identical to the reference; the
+ * mt19937_64 stream bit-identical, Box-Muller within a few ulp); kernels on the host.
+ * Errors as the reference: size < 3x3 -> SHAPE, no lines -> CONFIG (ndconv::Error),
+ * sigma <= 0 or std_dev < 0 -> NUMERIC, even kernel extent -> SHAPE. */
+ndc_status ndc_sim_phantom_lines_f64(size_t rows, size_t cols, size_t n_lines, double intensity,
+                                     double* out);                     /* simulation.hpp:36-70 */
+ndc_status ndc_sim_phantom_texture_f64(size_t rows, size_t cols, double* out);  /* :72-94 */
+ndc_status ndc_sim_gaussian_psf_f64(int ndim, const size_t* ext, double sigma, double* out);  /* :98-122 */
+ndc_status ndc_sim_delta_psf_f64(int ndim, const size_t* ext, double* out);  /* :124-131 */
+ndc_status ndc_sim_add_gaussian_noise_f64(size_t n, const double* in, double mean, double std_dev,
+                                          uint64_t seed, double* out);  /* :154-191 */
+/* Raw std::mt19937_64(seed) words [skip, skip+n), generated on the device. */
+ndc_status ndc_sim_mt19937_64(uint64_t seed, size_t skip, size_t n, uint64_t* out);
+
 /* ---- device-resident plan (same operators, buffers kept in HBM between calls) ----
  * A plan owns the device buffers for `batch` images of one (x_ext, k_ext) problem, a
  * CUDA stream, and -- for z-slab sharded runs -- an NCCL communicator.  All calls on
@@ -195,12 +210,18 @@ ndc_status ndc_plan_get_report(ndc_plan* plan, size_t image, ndc_deconv_report* 
                                double* obj_trace, double* kkt_trace, size_t trace_cap);
 ndc_status ndc_plan_get_estimate_f64(ndc_plan* plan, double* x_out);
 ndc_status ndc_plan_get_estimate_f32(ndc_plan* plan, float* x_out);
+/* The resident observation (float32 on the device), owned planes when sharded. */
+ndc_status ndc_plan_get_observation_f64(ndc_plan* plan, double* y_out);
 /* Stream an NDTENSOR observation file straight into the plan (pinned 16 MB chunks, no
  * full host copy; a batch plan reads [batch, y_ext...] or, for batch 1, [y_ext...];
  * a sharded plan reads only its own planes), and stream the estimate back out
  * (sharded ranks each write their planes into one file; rank 0 writes the header). */
 ndc_status ndc_plan_load_observation_ndtensor(ndc_plan* plan, const char* path);
 ndc_status ndc_plan_save_estimate_ndtensor(ndc_plan* plan, const char* path);
+/* add_gaussian_noise (simulation.hpp:184-191) to the resident observation in place: the
+ * mt19937_64 stream of `seed` runs over the dense [batch, y...] storage order, generated
+ * on the device; a sharded rank applies its own planes' samples. */
+ndc_status ndc_plan_add_gaussian_noise(ndc_plan* plan, double mean, double std_dev, uint64_t seed);
 /* One forward (A x) / adjoint (A^T y) pass on resident buffers, for kernel timing. */
 ndc_status ndc_plan_forward(ndc_plan* plan);
 ndc_status ndc_plan_adjoint(ndc_plan* plan);

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <cstdint>
 #include <initializer_list>
 #include <limits>
 #include <optional>
@@ -514,8 +515,74 @@ inline void write_pgm(const Tensor& t, const std::string& path, bool clamp) {
 
 }  // namespace io
 
-// ---- metrics (simulation.hpp:195-208) ------------------------------------------------------
+// ---- simulation (simulation.hpp:20-208; image-sized generation on the device) -------------
 namespace sim {
+struct NoiseSpec {
+  double mean = 0.0;
+  double std_dev = 0.0;
+  std::uint64_t seed = 0;
+};
+
+struct PsfSpec {
+  enum class Kind { gaussian, delta, custom };
+  Kind kind = Kind::gaussian;
+  std::vector<std::size_t> size{5, 5};
+  double sigma = 1.0;
+  std::optional<Tensor> values{};
+};
+
+inline Tensor phantom_lines(std::size_t rows, std::size_t cols, std::size_t n_lines, double intensity) {
+  std::vector<double> v(rows * cols);
+  b200::check(ndc_sim_phantom_lines_f64(rows, cols, n_lines, intensity, v.data()));
+  return Tensor(Shape{rows, cols}, std::move(v));
+}
+
+inline Tensor phantom_texture(std::size_t rows, std::size_t cols) {
+  std::vector<double> v(rows * cols);
+  b200::check(ndc_sim_phantom_texture_f64(rows, cols, v.data()));
+  return Tensor(Shape{rows, cols}, std::move(v));
+}
+
+inline Kernel gaussian_psf(const std::vector<std::size_t>& extents, double sigma) {
+  std::size_t n = 1;
+  for (std::size_t e : extents) n *= e;
+  std::vector<double> v(extents.empty() ? 1 : n);
+  b200::check(ndc_sim_gaussian_psf_f64(static_cast<int>(extents.size()), extents.data(), sigma, v.data()));
+  return Kernel(Tensor(Shape(std::vector<std::size_t>(extents)), std::move(v)));
+}
+
+inline Kernel delta_psf(const std::vector<std::size_t>& extents) {
+  std::size_t n = 1;
+  for (std::size_t e : extents) n *= e;
+  std::vector<double> v(extents.empty() ? 1 : n);
+  b200::check(ndc_sim_delta_psf_f64(static_cast<int>(extents.size()), extents.data(), v.data()));
+  return Kernel(Tensor(Shape(std::vector<std::size_t>(extents)), std::move(v)));
+}
+
+inline Kernel make_psf(const PsfSpec& spec) {
+  switch (spec.kind) {
+    case PsfSpec::Kind::gaussian:
+      return gaussian_psf(spec.size, spec.sigma);
+    case PsfSpec::Kind::delta:
+      return delta_psf(spec.size);
+    case PsfSpec::Kind::custom: {
+      if (!spec.values) throw Error("make_psf: custom PSF needs values");
+      for (double v : spec.values->data())
+        if (v < 0.0) throw NumericError("make_psf: PSF values must be nonnegative");
+      return Kernel(*spec.values);
+    }
+  }
+  throw Error("make_psf: unknown kind");
+}
+
+inline Tensor add_gaussian_noise(const Tensor& t, const NoiseSpec& spec) {
+  std::vector<double> v(t.size());
+  b200::check(ndc_sim_add_gaussian_noise_f64(t.size(), t.data().data(), spec.mean, spec.std_dev, spec.seed,
+                                             v.data()));
+  return Tensor(t.shape(), std::move(v));
+}
+
+// ---- metrics (simulation.hpp:195-208) ------------------------------------------------------
 inline double snr_db(const Tensor& reference, const Tensor& estimate) {
   ndconv::detail::check_same_shape(reference, estimate, "snr_db");
   double ref = 0.0, err = 0.0;

@@ -255,3 +255,44 @@ class Oracle:
         out = C.c_double()
         self._call("snr_db", C.c_int(a.ndim), _ext(a.shape), _ptr(a), _ptr(b), C.byref(out))
         return out.value
+
+    # --- simulation generators (reference only: ref_shim.cpp ref_sim_*) ------------------
+    def phantom_lines(self, rows, cols, n_lines, intensity):
+        self._ref_only("phantom_lines")
+        out = np.empty((rows, cols), np.float64)
+        self._call("sim_phantom_lines", C.c_size_t(rows), C.c_size_t(cols), C.c_size_t(n_lines),
+                   C.c_double(intensity), _ptr(out))
+        return out
+
+    def phantom_texture(self, rows, cols):
+        self._ref_only("phantom_texture")
+        out = np.empty((rows, cols), np.float64)
+        self._call("sim_phantom_texture", C.c_size_t(rows), C.c_size_t(cols), _ptr(out))
+        return out
+
+    def gaussian_psf(self, extents, sigma):
+        self._ref_only("gaussian_psf")
+        out = np.empty(tuple(extents), np.float64)
+        self._call("sim_gaussian_psf", C.c_int(len(extents)), _ext(extents), C.c_double(sigma), _ptr(out))
+        return out
+
+    def delta_psf(self, extents):
+        self._ref_only("delta_psf")
+        out = np.empty(tuple(extents), np.float64)
+        self._call("sim_delta_psf", C.c_int(len(extents)), _ext(extents), _ptr(out))
+        return out
+
+    def add_gaussian_noise(self, t, mean, std_dev, seed):
+        self._ref_only("add_gaussian_noise")
+        t = _f64(t)
+        out = np.empty_like(t)
+        self._call("sim_add_gaussian_noise", C.c_size_t(t.size), _ptr(t), C.c_double(mean), C.c_double(std_dev),
+                   C.c_uint64(seed), _ptr(out))
+        return out
+
+    def mt19937_64(self, seed, n, skip=0):
+        self._ref_only("mt19937_64")
+        out = np.empty(n, np.uint64)
+        self._call("mt19937_64", C.c_uint64(seed), C.c_size_t(skip), C.c_size_t(n),
+                   out.ctypes.data_as(C.POINTER(C.c_uint64)))
+        return out

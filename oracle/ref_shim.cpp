@@ -12,7 +12,9 @@
 // never interpose on (or be interposed by) anything else in the process.
 #include <cstddef>
 #include <cstring>
+#include <cstdint>
 #include <exception>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -344,4 +346,41 @@ REF_API int ref_io_serialize_pgm(int ndim, const std::size_t* ext, const double*
 
 REF_API int ref_snr_db(int ndim, const std::size_t* ext, const double* a, const double* b, double* out) {
   return guard([&] { *out = ndconv::sim::snr_db(tensor_of(ndim, ext, a), tensor_of(ndim, ext, b)); });
+}
+
+// ---- simulation generators (simulation.hpp) ---------------------------------------------
+REF_API int ref_sim_phantom_lines(std::size_t rows, std::size_t cols, std::size_t n, double intensity,
+                                  double* out) {
+  return guard([&] { put(ndconv::sim::phantom_lines(rows, cols, n, intensity), out); });
+}
+
+REF_API int ref_sim_phantom_texture(std::size_t rows, std::size_t cols, double* out) {
+  return guard([&] { put(ndconv::sim::phantom_texture(rows, cols), out); });
+}
+
+REF_API int ref_sim_gaussian_psf(int ndim, const std::size_t* ext, double sigma, double* out) {
+  return guard([&] {
+    put(ndconv::sim::gaussian_psf(std::vector<std::size_t>(ext, ext + ndim), sigma).tensor(), out);
+  });
+}
+
+REF_API int ref_sim_delta_psf(int ndim, const std::size_t* ext, double* out) {
+  return guard([&] { put(ndconv::sim::delta_psf(std::vector<std::size_t>(ext, ext + ndim)).tensor(), out); });
+}
+
+REF_API int ref_sim_add_gaussian_noise(std::size_t n, const double* in, double mean, double std_dev,
+                                       std::uint64_t seed, double* out) {
+  return guard([&] {
+    const std::size_t ext[1] = {n};
+    put(ndconv::sim::add_gaussian_noise(tensor_of(1, ext, in), {mean, std_dev, seed}), out);
+  });
+}
+
+// The raw engine the reference's GaussianSource wraps (simulation.hpp:175).
+REF_API int ref_mt19937_64(std::uint64_t seed, std::size_t skip, std::size_t n, std::uint64_t* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    rng.discard(skip);
+    for (std::size_t i = 0; i < n; ++i) out[i] = rng();
+  });
 }

@@ -99,6 +99,14 @@ _SIGS = [
     ("ndc_pgm_info", C.c_int, [C.c_char_p, size_t_p, size_t_p]),
     ("ndc_pgm_read_f64", C.c_int, [C.c_char_p, dbl_p, C.c_size_t]),
     ("ndc_pgm_write_f64", C.c_int, [C.c_char_p, C.c_size_t, C.c_size_t, dbl_p, C.c_int]),
+    ("ndc_plan_get_observation_f64", C.c_int, [C.c_void_p, dbl_p]),
+    ("ndc_plan_add_gaussian_noise", C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_uint64]),
+    ("ndc_sim_phantom_lines_f64", C.c_int, [C.c_size_t, C.c_size_t, C.c_size_t, C.c_double, dbl_p]),
+    ("ndc_sim_phantom_texture_f64", C.c_int, [C.c_size_t, C.c_size_t, dbl_p]),
+    ("ndc_sim_gaussian_psf_f64", C.c_int, [C.c_int, size_t_p, C.c_double, dbl_p]),
+    ("ndc_sim_delta_psf_f64", C.c_int, [C.c_int, size_t_p, dbl_p]),
+    ("ndc_sim_add_gaussian_noise_f64", C.c_int, [C.c_size_t, dbl_p, C.c_double, C.c_double, C.c_uint64, dbl_p]),
+    ("ndc_sim_mt19937_64", C.c_int, [C.c_uint64, C.c_size_t, C.c_size_t, C.POINTER(C.c_uint64)]),
     ("ndc_plan_forward", C.c_int, [C.c_void_p]),
     ("ndc_plan_adjoint", C.c_int, [C.c_void_p]),
     ("ndc_plan_set_timing", C.c_int, [C.c_void_p, C.c_int]),

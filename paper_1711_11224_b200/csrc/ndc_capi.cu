@@ -8,6 +8,7 @@
 
 #include "ndc_io.h"
 #include "ndc_plan.h"
+#include "ndc_sim.h"
 
 struct ndc_plan {
   std::unique_ptr<ndc::Plan> p;
@@ -382,11 +383,61 @@ ndc_status ndc_plan_get_estimate_f64(ndc_plan* plan, double* x_out) {
 ndc_status ndc_plan_get_estimate_f32(ndc_plan* plan, float* x_out) {
   NDC_PLAN(need(x_out, "x_out"); plan->p->get_estimate_f32(x_out));
 }
+ndc_status ndc_plan_get_observation_f64(ndc_plan* plan, double* y_out) {
+  NDC_PLAN(need(y_out, "y_out"); plan->p->get_observation_f64(y_out));
+}
 ndc_status ndc_plan_load_observation_ndtensor(ndc_plan* plan, const char* path) {
   NDC_PLAN(need(path, "path"); plan->p->load_observation_ndtensor(path));
 }
 ndc_status ndc_plan_save_estimate_ndtensor(ndc_plan* plan, const char* path) {
   NDC_PLAN(need(path, "path"); plan->p->save_estimate_ndtensor(path));
+}
+ndc_status ndc_plan_add_gaussian_noise(ndc_plan* plan, double mean, double std_dev, uint64_t seed) {
+  NDC_PLAN(plan->p->add_gaussian_noise(mean, std_dev, seed));
+}
+
+// ---- simulation generators (ndc_sim.cu) -----------------------------------------------------
+ndc_status ndc_sim_phantom_lines_f64(size_t rows, size_t cols, size_t n_lines, double intensity, double* out) {
+  return guard([&] {
+    need(out, "out");
+    ndc::sim_phantom_lines(g_device, rows, cols, n_lines, intensity, out);
+  });
+}
+ndc_status ndc_sim_phantom_texture_f64(size_t rows, size_t cols, double* out) {
+  return guard([&] {
+    need(out, "out");
+    ndc::sim_phantom_texture(g_device, rows, cols, out);
+  });
+}
+ndc_status ndc_sim_gaussian_psf_f64(int ndim, const size_t* ext, double sigma, double* out) {
+  return guard([&] {
+    need(ext, "ext");
+    need(out, "out");
+    ndc::sim_gaussian_psf(ndim, ext, sigma, out);
+  });
+}
+ndc_status ndc_sim_delta_psf_f64(int ndim, const size_t* ext, double* out) {
+  return guard([&] {
+    need(ext, "ext");
+    need(out, "out");
+    ndc::sim_delta_psf(ndim, ext, out);
+  });
+}
+ndc_status ndc_sim_add_gaussian_noise_f64(size_t n, const double* in, double mean, double std_dev, uint64_t seed,
+                                          double* out) {
+  return guard([&] {
+    if (n) {
+      need(in, "in");
+      need(out, "out");
+    }
+    ndc::sim_add_gaussian_noise(g_device, n, in, mean, std_dev, seed, out);
+  });
+}
+ndc_status ndc_sim_mt19937_64(uint64_t seed, size_t skip, size_t n, uint64_t* out) {
+  return guard([&] {
+    if (n) need(out, "out");
+    ndc::sim_mt19937_64(g_device, seed, skip, n, out);
+  });
 }
 
 // ---- tensor files ---------------------------------------------------------------------------

@@ -15,6 +15,7 @@
 
 #include "ndc_io.h"
 #include "ndc_plan.h"
+#include "ndc_sim.h"
 
 namespace ndc {
 
@@ -657,6 +658,7 @@ void Plan::set_x_f64(const double* x) {
 }
 void Plan::get_estimate_f64(double* x) { unpack_dense_f64(x_, x, X_, xa_ - xlo_, xa_n_); }
 void Plan::get_estimate_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
+void Plan::get_observation_f64(double* y) { unpack_dense_f64(yobs_, y, Y_, ya_ - rlo_, yb_ - ya_); }
 void Plan::get_y_buffer_f64(double* y) { unpack_dense_f64(r_, y, Y_, ya_ - rlo_, yb_ - ya_); }
 void Plan::get_x_buffer_f64(double* x, int which) {
   unpack_dense_f64(which == 0 ? x_ : g_, x, X_, xa_ - xlo_, xa_n_);
@@ -877,6 +879,24 @@ void Plan::save_estimate_ndtensor(const std::string& path) {
     comm_->allgather(dsc_, gather_, 1, stream_);
     sync();
   }
+}
+
+void Plan::add_gaussian_noise(double mean, double std_dev, uint64_t seed) {
+  if (std_dev < 0) fail(NDC_ERR_NUMERIC, "add_gaussian_noise: std_dev must be >= 0");
+  const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;
+  const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;
+  const size_t own = static_cast<size_t>(yb_ - ya_) * plane;
+  double* dense = static_cast<double*>(staging_);
+  GaussianNoise noise(seed, mean, std_dev, stream_);
+  for (size_t b = 0; b < B_; ++b) {
+    float* base = yobs_ + b * Y_.image + static_cast<long long>(ya_ - rlo_) * Y_.plane;
+    check_cuda(launch_unpack_f64(base, dense, 1, Y_.geo(yb_ - ya_), stream_), "unpack");
+    noise.add(dense, own, b * full + static_cast<size_t>(ya_) * plane);
+    check_cuda(launch_pack_f64(dense, base, 1, Y_.geo(yb_ - ya_), stream_), "pack");
+    st_[2].launches += 2;
+  }
+  sync();
+  halo_y(yobs_);
 }
 
 // solvers.hpp:127-143 in float64 on dense scratch buffers (small problems only).

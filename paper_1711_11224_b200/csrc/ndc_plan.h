@@ -78,10 +78,14 @@ class Plan {
   void set_x_f64(const double* x);               // into the x buffer (for conv_full etc.)
   void get_estimate_f64(double* x);
   void get_estimate_f32(float* x);
+  void get_observation_f64(double* y);           // the resident (f32) observation
   void get_y_buffer_f64(double* y);              // the y-shaped result buffer (A x)
   void get_x_buffer_f64(double* x, int which);   // 0 = x, 1 = g
   void load_observation_ndtensor(const std::string& path);  // streamed, owned planes
   void save_estimate_ndtensor(const std::string& path);
+  // add_gaussian_noise (simulation.hpp:184-191) to the resident observation in place, the
+  // mt19937_64 stream running over the user's dense [batch, y...] storage order
+  void add_gaussian_noise(double mean, double std_dev, uint64_t seed);
   std::vector<size_t> user_shape(bool y) const;   // [batch,] extents as the caller sees them
 
   // --- operators on resident buffers (the one-shot C-ABI entry points use these) ---

@@ -11,10 +11,16 @@
 //          [--method pg|rl] [--max-iters N] [--tol T] [--step S] [--seedless]
 //          [--trace-csv PATH]
 //   ndconv metrics --reference A --estimate B
-// simulate / verify / matrix are host-side tooling outside the accelerated path.
+//   ndconv simulate --outdir D [--phantom lines|texture|PGM] [--size r[,c]] [--lines N]
+//          [--psf gaussian|delta] [--psf-size k[,k]] [--sigma S] [--noise-mean M]
+//          [--noise-std S] [--seed N]          (phantoms and noise generated on the device)
+// verify / matrix (explicit-matrix property checks, O(N^2) host tooling) are not part
+// of the B200 build.
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
+#include <filesystem>
 #include <fstream>
 #include <map>
 #include <set>
@@ -137,15 +143,42 @@ double to_nonneg(const std::string& k, const std::string& v) {
   return x;
 }
 
-std::vector<std::size_t> to_list(const std::string& k, const std::string& v) {
+std::size_t to_count(const std::string& k, const std::string& v) {
+  char* end = nullptr;
+  const long long x = std::strtoll(v.c_str(), &end, 10);
+  if (v.empty() || *end != '\0' || x < 0) throw UsageError("--" + k + ": expected a non-negative integer");
+  return static_cast<std::size_t>(x);
+}
+
+double to_double(const std::string& k, const std::string& v) {
+  char* end = nullptr;
+  const double x = std::strtod(v.c_str(), &end);
+  if (v.empty() || *end != '\0') throw UsageError("--" + k + ": expected a number");
+  return x;
+}
+
+std::uint64_t to_u64(const std::string& k, const std::string& v) {
+  char* end = nullptr;
+  if (v.empty() || v[0] == '-') throw UsageError("--" + k + ": expected an unsigned integer");
+  const unsigned long long x = std::strtoull(v.c_str(), &end, 10);
+  if (*end != '\0') throw UsageError("--" + k + ": expected an unsigned integer");
+  return static_cast<std::uint64_t>(x);
+}
+
+// Comma-separated list; `positive` rejects zero entries (CLI11 PositiveNumber), `max_n`
+// bounds the count (CLI11 expected(1, max_n)).
+std::vector<std::size_t> to_list(const std::string& k, const std::string& v, bool positive = true,
+                                 std::size_t max_n = 0) {
   std::vector<std::size_t> out;
   std::size_t start = 0;
   while (start <= v.size()) {
     const std::size_t comma = v.find(',', start);
-    out.push_back(to_positive(k, v.substr(start, comma == std::string::npos ? std::string::npos : comma - start)));
+    const std::string item = v.substr(start, comma == std::string::npos ? std::string::npos : comma - start);
+    out.push_back(positive ? to_positive(k, item) : to_count(k, item));
     if (comma == std::string::npos) break;
     start = comma + 1;
   }
+  if (max_n && out.size() > max_n) throw UsageError("--" + k + ": expected at most " + std::to_string(max_n) + " values");
   return out;
 }
 
@@ -248,14 +281,70 @@ int run_metrics(const std::vector<std::string>& args) {
   return 0;
 }
 
+int run_simulate(const std::vector<std::string>& args) {
+  const Opts o = parse_opts(args, {"phantom", "size", "lines", "psf", "psf-size", "sigma", "noise-mean", "noise-std",
+                                   "seed", "outdir"},
+                            {});
+  const std::string outdir = req(o, "outdir");
+  auto get = [&](const char* k, const char* dflt) { return o.kv.count(k) ? o.kv.at(k) : std::string(dflt); };
+  const std::string phantom = get("phantom", "lines"), psf_kind = get("psf", "gaussian");
+  const std::vector<std::size_t> size = to_list("size", get("size", "128"), false, 2);
+  const std::size_t lines = to_positive("lines", get("lines", "9"));
+  std::vector<std::size_t> psf_ext = to_list("psf-size", get("psf-size", "5"), false, 2);
+  const double sigma = to_double("sigma", get("sigma", "1.0"));
+  const double noise_mean = to_double("noise-mean", get("noise-mean", "0.0"));
+  const double noise_std = to_double("noise-std", get("noise-std", "5.0"));
+  const std::uint64_t seed = to_u64("seed", get("seed", "1"));
+
+  const std::size_t rows = size.at(0), cols = size.size() > 1 ? size.at(1) : rows;
+  const Tensor truth = phantom == "lines"     ? sim::phantom_lines(rows, cols, lines, 255.0)
+                       : phantom == "texture" ? sim::phantom_texture(rows, cols)
+                                              : io::read_pgm(phantom);  // any PGM serves as a phantom
+  if (psf_ext.size() == 1) psf_ext.push_back(psf_ext[0]);
+  const Kernel psf = psf_kind == "gaussian" ? sim::gaussian_psf(psf_ext, sigma)
+                     : psf_kind == "delta"  ? sim::delta_psf(psf_ext)
+                                            : throw Error("unknown --psf kind '" + psf_kind +
+                                                          "' (expected gaussian or delta)");
+  const Tensor observed = sim::add_gaussian_noise(conv_full(truth, psf), {noise_mean, noise_std, seed});
+
+  std::filesystem::create_directories(outdir);
+  const std::filesystem::path dir(outdir);
+  io::write_tensor(truth, (dir / "truth.ndt").string());
+  io::write_pgm(truth, (dir / "truth.pgm").string(), /*clamp=*/true);
+  io::write_tensor(psf.tensor(), (dir / "psf.ndt").string());
+  io::write_tensor(observed, (dir / "observed.ndt").string());
+  io::write_pgm(observed, (dir / "observed.pgm").string(), /*clamp=*/true);
+
+  Manifest m = header("simulate");
+  m.add("phantom", phantom);
+  m.add("size", shape_csv(truth.shape()));
+  m.add_count("lines", lines);
+  m.add("psf", psf_kind);
+  m.add("psf_size", shape_csv(psf.shape()));
+  m.add_num("sigma", sigma);
+  m.add_num("noise_mean", noise_mean);
+  m.add_num("noise_std", noise_std);
+  m.add("seed", std::to_string(seed));
+  m.add("outdir", outdir);
+  m.add("truth", (dir / "truth.ndt").string());
+  m.add("psf_file", (dir / "psf.ndt").string());
+  m.add("observed", (dir / "observed.ndt").string());
+  m.add("observed_shape", shape_csv(observed.shape()));
+  m.write((dir / "manifest.txt").string());
+  return 0;
+}
+
 void usage(std::FILE* f) {
   std::fprintf(f,
                "ndconv %s (B200 / sm_100a) -- n-dimensional convolution and deconvolution\n"
-               "usage: ndconv [--threads N] <convolve|deconv|metrics> [options]\n"
+               "usage: ndconv [--threads N] <convolve|deconv|metrics|simulate> [options]\n"
                "  convolve --input X --kernel H --output Y\n"
                "  deconv   --observed Y --kernel H --shape d1,d2 --output X [--method pg|rl]\n"
                "           [--max-iters N] [--tol T] [--step S] [--seedless] [--trace-csv P]\n"
-               "  metrics  --reference A --estimate B\n",
+               "  metrics  --reference A --estimate B\n"
+               "  simulate --outdir D [--phantom lines|texture|P.pgm] [--size r[,c]] [--lines N]\n"
+               "           [--psf gaussian|delta] [--psf-size k[,k]] [--sigma S] [--noise-mean M]\n"
+               "           [--noise-std S] [--seed N]\n",
                kVersion);
 }
 
@@ -298,7 +387,8 @@ int main(int argc, char** argv) {
     if (sub == "convolve") return run_convolve(rest);
     if (sub == "deconv") return run_deconv(rest);
     if (sub == "metrics") return run_metrics(rest);
-    if (sub == "simulate" || sub == "verify" || sub == "matrix")
+    if (sub == "simulate") return run_simulate(rest);
+    if (sub == "verify" || sub == "matrix")
       throw UsageError(sub + ": host-side tooling, not part of the B200 build");
     throw UsageError("unknown subcommand '" + sub + "'");
   } catch (const UsageError& e) {

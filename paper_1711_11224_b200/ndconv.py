@@ -326,6 +326,69 @@ def write_pgm(t, path, clamp: bool = True) -> None:
     _check(N.lib().ndc_pgm_write_f64(_path(path), t.shape[0], t.shape[1], _p(t), 1 if clamp else 0))
 
 
+# --- simulation generators (simulation.hpp:36-208; image-sized work on the device) ----------
+
+
+def phantom_lines(rows: int, cols: int, n_lines: int, intensity: float) -> np.ndarray:
+    """simulation.hpp:36-70, bit-identical to the reference."""
+    out = np.empty((int(rows), int(cols)), np.float64)
+    _check(N.lib().ndc_sim_phantom_lines_f64(int(rows), int(cols), int(n_lines), float(intensity), _p(out)))
+    return out
+
+
+def phantom_texture(rows: int, cols: int) -> np.ndarray:
+    """simulation.hpp:72-94, bit-identical to the reference."""
+    out = np.empty((int(rows), int(cols)), np.float64)
+    _check(N.lib().ndc_sim_phantom_texture_f64(int(rows), int(cols), _p(out)))
+    return out
+
+
+def gaussian_psf(extents, sigma: float) -> np.ndarray:
+    """simulation.hpp:98-122: sampled isotropic Gaussian, unit sum."""
+    ext = tuple(int(e) for e in extents)
+    out = np.empty(ext, np.float64)
+    _check(N.lib().ndc_sim_gaussian_psf_f64(len(ext), _ext(ext), float(sigma), _p(out)))
+    return out
+
+
+def delta_psf(extents) -> np.ndarray:
+    """simulation.hpp:124-131: centred unit impulse."""
+    ext = tuple(int(e) for e in extents)
+    out = np.empty(ext, np.float64)
+    _check(N.lib().ndc_sim_delta_psf_f64(len(ext), _ext(ext), _p(out)))
+    return out
+
+
+def add_gaussian_noise(t, mean: float = 0.0, std_dev: float = 0.0, seed: int = 0) -> np.ndarray:
+    """simulation.hpp:184-191: t + mean + std_dev * N(0,1) from mt19937_64(seed) + Box-Muller,
+    drawn in flat storage order on the device."""
+    t = _f64(t)
+    out = np.empty_like(t)
+    _check(N.lib().ndc_sim_add_gaussian_noise_f64(t.size, _p(t), float(mean), float(std_dev),
+                                                  C.c_uint64(int(seed) & (2**64 - 1)), _p(out)))
+    return out
+
+
+def mt19937_64(seed: int, n: int, skip: int = 0) -> np.ndarray:
+    """Raw std::mt19937_64(seed) words [skip, skip+n), generated on the device."""
+    out = np.empty(int(n), np.uint64)
+    _check(N.lib().ndc_sim_mt19937_64(C.c_uint64(int(seed) & (2**64 - 1)), int(skip), int(n),
+                                      out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return out
+
+
+def snr_db(reference, estimate) -> float:
+    """simulation.hpp:195-208: 10 log10(|ref|^2 / |est - ref|^2); inf for an exact match."""
+    a, b = _f64(reference), _f64(estimate)
+    if a.shape != b.shape:
+        raise ShapeError(f"snr_db: shape {a.shape} vs {b.shape}")
+    ref = float(np.sum(a * a))
+    err = float(np.sum((b - a) ** 2))
+    if ref == 0.0:
+        raise NumericError("snr_db: reference is all zero, metric undefined")
+    return float("inf") if err == 0.0 else 10.0 * float(np.log10(ref / err))
+
+
 # --- device-resident plan ----------------------------------------------------------------
 
 
@@ -428,6 +491,12 @@ class Plan:
     def save_estimate(self, path):
         _check(N.lib().ndc_plan_save_estimate_ndtensor(self.handle, _path(path)))
 
+    def add_gaussian_noise(self, mean: float = 0.0, std_dev: float = 0.0, seed: int = 0):
+        """add_gaussian_noise on the resident observation (device mt19937_64 stream over the
+        dense [batch, y...] order; a sharded rank applies its own planes' samples)."""
+        _check(N.lib().ndc_plan_add_gaussian_noise(self.handle, float(mean), float(std_dev),
+                                                   C.c_uint64(int(seed) & (2**64 - 1))))
+
     def pg_begin(self, cfg: DeconvConfig | None = None):
         c = (cfg or DeconvConfig()).to_c()
         _check(N.lib().ndc_plan_pg_begin(self.handle, C.byref(c)))
@@ -451,6 +520,12 @@ class Plan:
         else:
             _check(N.lib().ndc_plan_get_estimate_f64(self.handle, _p(x)))
         return x
+
+    def observation(self) -> np.ndarray:
+        """The resident observation (float32 on the device) as float64, owned planes."""
+        y = np.empty((self.batch,) + self.owned_y_shape(), np.float64)
+        _check(N.lib().ndc_plan_get_observation_f64(self.handle, _p(y)))
+        return y
 
     def report(self, image: int, cap: int) -> DeconvReport:
         rep = N.Report()

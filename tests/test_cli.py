@@ -13,6 +13,7 @@ import pytest
 from oracle import oracle as O
 from paper_1711_11224_b200 import build as B
 from paper_1711_11224_b200 import ndconv as nd
+from tests.conftest import rel_l2
 
 # main.cpp:161-179: the deconv manifest's keys, in order (trace_csv / final_kkt /
 # negative_pixels_clamped are conditional).
@@ -134,7 +135,7 @@ def test_convolve_delta_kernel_reproduces_input(cli, tmp_path, nd):
 
 
 @pytest.mark.gpu
-def test_convolve_matches_oracle(cli, tmp_path, nd, oracle_c, rel_l2):
+def test_convolve_matches_oracle(cli, tmp_path, nd, oracle_c):
     rng = np.random.default_rng(21)
     x, h = rng.uniform(0, 1, (37, 50)), rng.uniform(0, 1, (5, 7))
     nd.write_tensor(x, str(tmp_path / "x.ndt"))
@@ -172,7 +173,10 @@ def test_deconv_drives_objective_down_with_consistent_trace(cli, tmp_path, nd, o
     assert rc == 0, err
     m, order = manifest(tmp_path / "est.ndt.manifest")
     assert order == [k for k in DECONV_KEYS if k != "negative_pixels_clamped"]
-    assert m["method"] == "pg" and m["stop_reason"] == "max_iters" and m["seedless"] == "true"
+    # The reference (f64) runs all 500 iterations; the fp32 device iterate reaches its
+    # bitwise fixed point (trial == x, solvers.hpp:191) earlier on this noiseless case,
+    # after the objective has already collapsed -- see DESIGN.md "fp32 fixed point".
+    assert m["method"] == "pg" and m["stop_reason"] in ("max_iters", "converged") and m["seedless"] == "true"
     assert m["shape"] == "32,32" and m["max_iters"] == "500" and m["step"] == "8" and m["tol"] == "0"
     rows = open(tmp_path / "trace.csv").read().splitlines()
     assert rows[0] == "iter,objective,kkt"
@@ -208,15 +212,16 @@ def test_deconv_rl_conserves_flux(cli, tmp_path, nd, oracle_c):
 
 
 @pytest.mark.gpu
-def test_deconv_stalled_exits_numeric(cli, tmp_path, nd):
-    # A zero kernel: no trial decreases the objective, the line search stalls (exit 5),
-    # but the estimate and manifest are still written first (main.cpp:158-183).
+def test_deconv_numeric_failure_exits_5(cli, tmp_path, nd):
+    # An all-zero kernel is refused by deconv_pg with NumericError (the reference does the
+    # same, oracle check below) -> exit code 5, no estimate written (main.cpp:139-158).
     y = np.ones((6, 6))
     nd.write_tensor(y, str(tmp_path / "y.ndt"))
     nd.write_tensor(np.zeros((3, 3)), str(tmp_path / "h.ndt"))
     rc, _, _ = run(cli, ["deconv", "--observed", "y.ndt", "--kernel", "h.ndt", "--shape", "4,4", "--step", "1",
                          "--output", "e.ndt"], tmp_path)
-    m, _ = manifest(tmp_path / "e.ndt.manifest")
-    assert rc in (0, 5)
-    if m["stop_reason"] == "stalled":
-        assert rc == 5
+    assert rc == 5
+    assert not os.path.exists(tmp_path / "e.ndt.manifest")
+    with pytest.raises(O.OracleError) as e:
+        O.Oracle("c").deconv_pg(y, np.zeros((3, 3)), (4, 4), initial_step=1.0)
+    assert e.value.kind == "NumericError"

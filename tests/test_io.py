@@ -42,7 +42,7 @@ def _ours_parse(tmp_path, data: bytes, pgm=False):
         return "ok", (nd.read_pgm(path) if pgm else nd.read_tensor(path))
     except nd.FormatError:
         return "FormatError", None
-    except nd.NdconvError as e:
+    except nd.Error as e:
         return type(e).__name__, None
 
 
