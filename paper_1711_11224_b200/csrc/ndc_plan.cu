@@ -10,6 +10,9 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+#include <functional>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <cstdio>
 
@@ -208,49 +211,42 @@ float* Plan::dev_alloc_f(long long n) {
 }
 
 namespace {
-// Persistent host copy pool: splits a pageable <-> pinned memcpy across worker threads
-// (a single thread moves ~10 GB/s; the PCIe DMA it feeds is several times faster).
-class CopyPool {
+// Persistent host worker pool for the host side of transfers: pageable <-> pinned
+// memcpy (a single thread moves ~10 GB/s; the PCIe DMA it feeds is several times
+// faster) and parallel pread / pwrite of tensor files.
+class HostPool {
  public:
-  static CopyPool& get() {
-    static CopyPool pool;
+  static HostPool& get() {
+    static HostPool pool;
     return pool;
   }
-  void copy(void* dst, const void* src, size_t n) {
-    const unsigned parts = static_cast<unsigned>(std::min<size_t>(workers_.size() + 1, n >> 20));
+  unsigned width() const { return static_cast<unsigned>(workers_.size()) + 1; }
+  // Runs fn(0) .. fn(parts-1) concurrently (the caller takes part 0); fn must not throw.
+  void run(unsigned parts, const std::function<void(unsigned)>& fn) {
     if (parts <= 1) {
-      std::memcpy(dst, src, n);
+      fn(0);
       return;
     }
-    const size_t per = (n + parts - 1) / parts;
-    std::unique_lock<std::mutex> call(call_mu_);  // one parallel copy at a time
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel job at a time
     {
       std::lock_guard<std::mutex> lk(mu_);
-      for (unsigned i = 1; i < parts; ++i) {
-        const size_t lo = i * per, hi = std::min(n, lo + per);
-        if (lo < hi) {
-          jobs_.push_back({static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo});
-          ++pending_;
-        }
-      }
+      fn_ = &fn;
+      for (unsigned i = 1; i < parts; ++i) jobs_.push_back(i);
+      pending_ += parts - 1;
     }
     cv_.notify_all();
-    std::memcpy(dst, src, std::min(n, per));  // the caller takes part 0
+    fn(0);
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
   }
 
  private:
-  struct Job {
-    char* dst;
-    const char* src;
-    size_t n;
-  };
-  CopyPool() {
+  HostPool() {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    for (unsigned i = 0; i + 1 < std::min(hw, 16u); ++i) workers_.emplace_back([this] { run(); });
+    for (unsigned i = 0; i + 1 < std::min(hw, 16u); ++i) workers_.emplace_back([this] { loop(); });
   }
-  ~CopyPool() {
+  ~HostPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
@@ -258,30 +254,46 @@ class CopyPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
-  void run() {
+  void loop() {
     for (;;) {
-      Job j;
+      unsigned part;
+      const std::function<void(unsigned)>* fn;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
         if (stop_) return;
-        j = jobs_.back();
+        part = jobs_.back();
         jobs_.pop_back();
+        fn = fn_;
       }
-      std::memcpy(j.dst, j.src, j.n);
+      (*fn)(part);
       std::lock_guard<std::mutex> lk(mu_);
       if (--pending_ == 0) done_cv_.notify_all();
     }
   }
   std::vector<std::thread> workers_;
-  std::vector<Job> jobs_;
+  std::vector<unsigned> jobs_;
+  const std::function<void(unsigned)>* fn_ = nullptr;
   std::mutex mu_, call_mu_;
   std::condition_variable cv_, done_cv_;
   size_t pending_ = 0;
   bool stop_ = false;
 };
 
-void par_copy(void* dst, const void* src, size_t n) { CopyPool::get().copy(dst, src, n); }
+// Splits [0, n) into `parts` near-equal ranges.
+inline std::pair<size_t, size_t> part_range(size_t n, unsigned parts, unsigned i) {
+  const size_t per = (n + parts - 1) / parts;
+  return {std::min(n, i * per), std::min(n, (i + 1) * per)};
+}
+
+void par_copy(void* dst, const void* src, size_t n) {
+  const unsigned parts = static_cast<unsigned>(std::min<size_t>(HostPool::get().width(), n >> 20));
+  HostPool::get().run(std::max(1u, parts), [&](unsigned i) {
+    const auto r = part_range(n, std::max(1u, parts), i);
+    std::memcpy(static_cast<char*>(dst) + r.first, static_cast<const char*>(src) + r.first, r.second - r.first);
+  });
+}
+
 
 constexpr size_t kPinChunk = size_t(16) << 20;
 
@@ -751,31 +763,65 @@ double Plan::estimate_step(size_t power_iters) {
 
 // ---- NDTENSOR streaming (imageio.hpp:24-125 format) ----------------------------------------
 namespace {
-// First non-finite index in v[0, n) (n when none), checked by several threads.
-size_t first_nonfinite(const double* v, size_t n) {
-  const unsigned t = std::max(1u, std::min(8u, static_cast<unsigned>(n >> 18)));
-  std::vector<size_t> bad(t, n);
-  std::vector<std::thread> th;
-  const size_t per = (n + t - 1) / t;
-  for (unsigned i = 0; i < t; ++i)
-    th.emplace_back([&, i] {
-      const size_t lo = i * per, hi = std::min(n, lo + per);
-      for (size_t k = lo; k < hi; ++k)
-        if (!std::isfinite(v[k])) {
-          bad[i] = k;
-          return;
-        }
-    });
-  for (auto& x : th) x.join();
-  return *std::min_element(bad.begin(), bad.end());
+size_t first_nonfinite_serial(const double* v, size_t n) {
+  for (size_t k = 0; k < n; ++k)
+    if (!std::isfinite(v[k])) return k;
+  return n;
 }
 
-struct FileCloser {
-  std::FILE* f;
-  ~FileCloser() {
-    if (f) std::fclose(f);
+struct Fd {
+  int fd;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
   }
 };
+
+// Full-length pread / pwrite (they may transfer less than asked).
+bool pread_all(int fd, void* buf, size_t n, size_t off) {
+  char* p = static_cast<char*>(buf);
+  while (n) {
+    const ssize_t r = ::pread(fd, p, n, static_cast<off_t>(off));
+    if (r <= 0) return false;
+    p += r;
+    off += static_cast<size_t>(r);
+    n -= static_cast<size_t>(r);
+  }
+  return true;
+}
+
+bool pwrite_all(int fd, const void* buf, size_t n, size_t off) {
+  const char* p = static_cast<const char*>(buf);
+  while (n) {
+    const ssize_t r = ::pwrite(fd, p, n, static_cast<off_t>(off));
+    if (r <= 0) return false;
+    p += r;
+    off += static_cast<size_t>(r);
+    n -= static_cast<size_t>(r);
+  }
+  return true;
+}
+
+// One pinned chunk of n doubles at file offset `off`, split over the host pool: each
+// part is read (or written) and range-checked by its own thread.  Returns the first
+// non-finite element (n if none); `io_ok` reports short reads / failed writes.
+size_t chunk_io(bool write, int fd, double* buf, size_t n, size_t off, bool& io_ok) {
+  HostPool& pool = HostPool::get();
+  const unsigned parts = std::max(1u, std::min<unsigned>(pool.width(), static_cast<unsigned>(n >> 17)));
+  std::vector<size_t> bad(parts, n);
+  std::vector<char> ok(parts, 1);
+  pool.run(parts, [&](unsigned i) {
+    const auto r = part_range(n, parts, i);
+    const size_t cnt = r.second - r.first;
+    if (!write) ok[i] = pread_all(fd, buf + r.first, cnt * 8, off + r.first * 8);
+    if (ok[i]) {
+      const size_t k = first_nonfinite_serial(buf + r.first, cnt);
+      if (k < cnt) bad[i] = r.first + k;
+    }
+    if (write && bad[i] == n) ok[i] = pwrite_all(fd, buf + r.first, cnt * 8, off + r.first * 8);
+  });
+  io_ok = std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+  return *std::min_element(bad.begin(), bad.end());
+}
 }  // namespace
 
 std::vector<size_t> Plan::user_shape(bool y) const {
@@ -789,31 +835,30 @@ std::vector<size_t> Plan::user_shape(bool y) const {
   return e;
 }
 
+// Streams the owned planes of an NDTENSOR file into HBM: each 16 MB pinned chunk is read
+// and checked by the host pool while the previous chunk's H2D is in flight.
 void Plan::load_observation_ndtensor(const std::string& path) {
   const NdtHeader h = read_ndtensor_header(path);
   if (h.ext != user_shape(true))
     fail(NDC_ERR_SHAPE, "load_observation: file shape does not match the plan's observation shape");
   ensure_pinned();
-  std::FILE* f = std::fopen(path.c_str(), "rb");
-  if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path);
-  FileCloser fc{f};
+  Fd fd{::open(path.c_str(), O_RDONLY)};
+  if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path);
   const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;                       // dense
   const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;               // one image
   const size_t own = static_cast<size_t>(yb_ - ya_) * plane;
-  const size_t chunk = (size_t(16) << 20) / 8;
+  const size_t chunk = kPinChunk / 8;
   size_t i = 0;
   for (size_t b = 0; b < B_; ++b) {
     const size_t first = b * full + static_cast<size_t>(ya_) * plane;
-    if (std::fseek(f, static_cast<long>(h.payload_offset + first * 8), SEEK_SET) != 0)
-      fail(NDC_ERR_FORMAT, "read_tensor: seek failure");
     for (size_t off = 0; off < own; off += chunk, ++i) {
       const int s = static_cast<int>(i & 1);
       const size_t n = std::min(chunk, own - off);
       if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
       double* buf = static_cast<double*>(hpin_[s]);
-      if (std::fread(buf, 8, n, f) != n)
-        fail(NDC_ERR_FORMAT, "read_tensor: truncated payload at element " + std::to_string(first + off));
-      const size_t bad = first_nonfinite(buf, n);
+      bool io_ok = true;
+      const size_t bad = chunk_io(false, fd.fd, buf, n, h.payload_offset + (first + off) * 8, io_ok);
+      if (!io_ok) fail(NDC_ERR_FORMAT, "read_tensor: truncated payload at element " + std::to_string(first + off));
       if (bad < n)
         fail(NDC_ERR_FORMAT, "read_tensor: non-finite value at element " + std::to_string(first + off + bad));
       check_cuda(cudaMemcpyAsync(static_cast<double*>(staging_) + off, buf, n * 8, cudaMemcpyHostToDevice,
@@ -831,18 +876,18 @@ void Plan::load_observation_ndtensor(const std::string& path) {
   halo_y(yobs_);
 }
 
+// Streams the owned estimate planes out: the D2H of chunk k+1 overlaps the host pool's
+// check + pwrite of chunk k.  Sharded ranks write their own planes of one file.
 void Plan::save_estimate_ndtensor(const std::string& path) {
   const std::vector<size_t> ext = user_shape(false);
   const std::string hl = ndtensor_header_line(ext);
   const size_t plane = static_cast<size_t>(my_) * mx_;
   const size_t full = static_cast<size_t>(mz_) * plane;
   if (rank_ == 0) {  // header + full-size file, then every rank fills its planes
-    std::FILE* f = std::fopen(path.c_str(), "wb");
-    if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
-    FileCloser fc{f};
-    bool ok = std::fwrite(hl.data(), 1, hl.size(), f) == hl.size();
-    ok = ok && std::fseek(f, static_cast<long>(hl.size() + full * B_ * 8 - 1), SEEK_SET) == 0;
-    ok = ok && std::fputc(0, f) != EOF;
+    Fd fd{::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644)};
+    if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
+    bool ok = pwrite_all(fd.fd, hl.data(), hl.size(), 0);
+    ok = ok && ::ftruncate(fd.fd, static_cast<off_t>(hl.size() + full * B_ * 8)) == 0;
     if (!ok) fail(NDC_ERR_FORMAT, "write_tensor: stream failure");
   }
   if (world_ > 1) {  // barrier: the file exists before the other ranks open it
@@ -850,29 +895,40 @@ void Plan::save_estimate_ndtensor(const std::string& path) {
     sync();
   }
   ensure_pinned();
-  std::FILE* f = std::fopen(path.c_str(), "r+b");
-  if (!f) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
-  FileCloser fc{f};
+  Fd fd{::open(path.c_str(), O_WRONLY)};
+  if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
   const size_t own = static_cast<size_t>(xa_n_) * plane;
-  const size_t chunk = (size_t(16) << 20) / 8;
+  const size_t chunk = kPinChunk / 8;
+  const size_t nchunks = (own + chunk - 1) / chunk;
   for (size_t b = 0; b < B_; ++b) {
     check_cuda(launch_unpack_f64(x_owned(x_) + b * X_.image, static_cast<double*>(staging_), 1,
                                  X_.geo(xa_n_), stream_),
                "unpack");
     st_[2].launches++;
     const size_t first = b * full + static_cast<size_t>(xa_) * plane;
-    if (std::fseek(f, static_cast<long>(hl.size() + first * 8), SEEK_SET) != 0)
-      fail(NDC_ERR_FORMAT, "write_tensor: seek failure");
-    for (size_t off = 0; off < own; off += chunk) {
-      const size_t n = std::min(chunk, own - off);
-      double* buf = static_cast<double*>(hpin_[0]);
-      check_cuda(cudaMemcpyAsync(buf, static_cast<const double*>(staging_) + off, n * 8,
+    auto d2h = [&](size_t k) {
+      const size_t n = std::min(chunk, own - k * chunk);
+      check_cuda(cudaMemcpyAsync(hpin_[k & 1], static_cast<const double*>(staging_) + k * chunk, n * 8,
                                  cudaMemcpyDeviceToHost, stream_),
                  "D2H");
-      sync();
-      if (first_nonfinite(buf, n) < n)
+      check_cuda(cudaEventRecord(pin_ev_[k & 1], stream_), "cudaEventRecord");
+    };
+    d2h(0);
+    for (size_t k = 0; k < nchunks; ++k) {
+      if (k + 1 < nchunks) d2h(k + 1);
+      check_cuda(cudaEventSynchronize(pin_ev_[k & 1]), "cudaEventSynchronize");
+      const size_t n = std::min(chunk, own - k * chunk);
+      bool io_ok = true;
+      const size_t bad = chunk_io(true, fd.fd, static_cast<double*>(hpin_[k & 1]), n,
+                                  hl.size() + (first + k * chunk) * 8, io_ok);
+      if (bad < n) {
+        sync();
         fail(NDC_ERR_NUMERIC, "write_tensor: refusing to store non-finite values");
-      if (std::fwrite(buf, 8, n, f) != n) fail(NDC_ERR_FORMAT, "write_tensor: stream failure");
+      }
+      if (!io_ok) {
+        sync();
+        fail(NDC_ERR_FORMAT, "write_tensor: stream failure");
+      }
     }
   }
   if (world_ > 1) {  // every rank's planes are on disk before any returns
