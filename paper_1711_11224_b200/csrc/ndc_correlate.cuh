@@ -83,117 +83,231 @@ __host__ __device__ constexpr int stage_bytes_aligned(int rows, int pitch_s) {
   return ((rows * pitch_s * 4) + 127) / 128 * 128;
 }
 
+// Epilogue staging: a dedicated 2 KB (32 rows x 16 floats) buffer per warp after the
+// stages, so no warp ever waits for another around the epilogue.
+constexpr int kStagingBytes = (kThreads / 32) * 32 * kRX * 4;
+
+// Dynamic shared memory: stages, staging, then the stage mbarriers.
+__host__ __device__ constexpr int barrier_offset(int stages, int sbytes) { return stages * sbytes + kStagingBytes; }
+
 // p0 combines with max for the KKT-style epilogues, with + otherwise.
 __device__ __forceinline__ bool p0_is_max(int mode) { return mode == kEpiPG || mode == kEpiKKT; }
 
-// Epilogue for one 16-wide output strip at buffer offset o (see EpiMode).
-__device__ __forceinline__ void epilogue_strip(const CorrGeom& g, const CorrArgs& a, int b,
-                                               long long o, int ox0, float* acc, double& p0,
-                                               double& p1) {
-  if (g.accum) {
+// Swizzled position of quad q of row r in a per-warp 32 x 16-float staging buffer:
+// XOR by (r >> 1) & 3 makes both the row-per-lane writes and the 4-lanes-per-row reads
+// of store_rows bank-conflict free.
+__device__ __forceinline__ int stage_pos(int r, int q) { return r * kRX + 4 * (q ^ ((r >> 1) & 3)); }
+
+// Epilogue value for `out` of quad q (4 columns) of one output row from the final
+// accumulators acc4 and the staged aux_in quad `in` (see EpiMode); reduction terms into
+// p0 / p1.  Columns past the valid extent are zero and excluded from the reductions.
+// MODE < 0: an intermediate tap chunk (the raw partial sum).
+template <int MODE>
+__device__ __forceinline__ float4 epilogue_res(int cols_left, const float* acc4, const float* in, float sc,
+                                               float step, double& p0, double& p1) {
+  float res[4];
 #pragma unroll
-    for (int q = 0; q < kRX / 4; ++q) {
-      const float4 p = *reinterpret_cast<const float4*>(a.accum_in + o + 4 * q);
-      acc[4 * q + 0] += p.x;
-      acc[4 * q + 1] += p.y;
-      acc[4 * q + 2] += p.z;
-      acc[4 * q + 3] += p.w;
-    }
-  }
-  if (!g.final_chunk) {
-#pragma unroll
-    for (int q = 0; q < kRX / 4; ++q)
-      *reinterpret_cast<float4*>(a.out + o + 4 * q) =
-          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-    return;
-  }
-  const int mode = g.mode;
-  const float sc = (a.scale != nullptr) ? a.scale[b] : 1.0f;
-  float res[kRX];
-  float aux[kRX];
-  float in[kRX];
-  if (mode == kEpiResid || mode == kEpiPG || mode == kEpiKKT || mode == kEpiRLRatio ||
-      mode == kEpiRLUpdate) {
-#pragma unroll
-    for (int q = 0; q < kRX / 4; ++q) {
-      const float4 v = *reinterpret_cast<const float4*>(a.aux_in + o + 4 * q);
-      in[4 * q] = v.x;
-      in[4 * q + 1] = v.y;
-      in[4 * q + 2] = v.z;
-      in[4 * q + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < kRX; ++c) in[c] = 0.f;
-  }
-  // The mode is uniform per launch: one specialised loop per mode (no per-element
-  // branching).  Columns past the valid extent are written as zero.
-#define NDC_EPI_LOOP(BODY)                           \
-  _Pragma("unroll") for (int c = 0; c < kRX; ++c) {  \
-    const bool ok = ox0 + c < g.out_ex;              \
-    float v = 0.f, ax = 0.f;                         \
-    BODY;                                            \
-    res[c] = ok ? v : 0.f;                           \
-    aux[c] = ok ? ax : 0.f;                          \
-  }
-  switch (mode) {
-    case kEpiStore:
-      NDC_EPI_LOOP(v = acc[c] * sc)
-      break;
-    case kEpiResid:
-      NDC_EPI_LOOP(v = acc[c] - in[c]; if (ok) p0 += static_cast<double>(v) * static_cast<double>(v))
-      break;
-    case kEpiNorm:
-      NDC_EPI_LOOP(v = acc[c] * sc; if (ok) p0 += static_cast<double>(v) * static_cast<double>(v))
-      break;
-    case kEpiPG: {
-      // solvers.hpp:180-191: g, kkt = max|min(x,g)|, trial = max(x - step*g, 0), and the
-      // bitwise fixed-point test trial == x.
-      const float step = static_cast<float>(a.step[b]);
-      NDC_EPI_LOOP(const float gg = acc[c]; const float xv = in[c];
-                   float t = __fsub_rn(xv, __fmul_rn(gg, step)); t = t < 0.f ? 0.f : t; v = t; ax = gg;
-                   if (ok) {
-                     p0 = fmax(p0, fabs(static_cast<double>(fminf(xv, gg))));
-                     p1 += (t != xv) ? 1.0 : 0.0;
-                   })
-      break;
-    }
-    case kEpiKKT:
-      NDC_EPI_LOOP(if (ok) p0 = fmax(p0, fabs(static_cast<double>(fminf(in[c], acc[c])))))
-      break;
-    case kEpiClamp:
-      NDC_EPI_LOOP(v = acc[c] < 0.f ? 0.f : acc[c])
-      break;
-    case kEpiRLRatio:
+  for (int c = 0; c < 4; ++c) {
+    const bool ok = c < cols_left;
+    const float acc_c = acc4[c];
+    float v = 0.f;
+    if (MODE < 0) {
+      v = acc_c;
+    } else if (MODE == kEpiStore) {
+      v = acc_c * sc;
+    } else if (MODE == kEpiResid) {
+      v = acc_c - in[c];
+      if (ok) p0 += static_cast<double>(v) * static_cast<double>(v);
+    } else if (MODE == kEpiNorm) {
+      v = acc_c * sc;
+      if (ok) p0 += static_cast<double>(v) * static_cast<double>(v);
+    } else if (MODE == kEpiPG) {
+      // solvers.hpp:180-191: kkt = max|min(x,g)|, trial = max(x - step*g, 0), and the
+      // bitwise fixed-point test trial == x (g itself is the aux output).
+      const float gg = acc_c, xv = in[c];
+      float t = __fsub_rn(xv, __fmul_rn(gg, step));
+      t = t < 0.f ? 0.f : t;
+      v = t;
+      if (ok) {
+        p0 = fmax(p0, fabs(static_cast<double>(fminf(xv, gg))));
+        p1 += (t != xv) ? 1.0 : 0.0;
+      }
+    } else if (MODE == kEpiKKT) {
+      if (ok) p0 = fmax(p0, fabs(static_cast<double>(fminf(in[c], acc_c))));
+    } else if (MODE == kEpiClamp) {
+      v = acc_c < 0.f ? 0.f : acc_c;
+    } else if (MODE == kEpiRLRatio) {
       // tensor.hpp:112-116 guarded_div(y, A x) fused with the residual A x - y.
-      NDC_EPI_LOOP(const float ax_v = acc[c] * sc; v = fabsf(ax_v) < 1e-12f ? 0.f : in[c] / ax_v;
-                   ax = ax_v - in[c]; if (ok) p0 += static_cast<double>(ax) * static_cast<double>(ax))
-      break;
-    case kEpiRLUpdate:
+      const float ax_v = acc_c * sc;
+      v = fabsf(ax_v) < 1e-12f ? 0.f : in[c] / ax_v;
+      const float d = ax_v - in[c];
+      if (ok) p0 += static_cast<double>(d) * static_cast<double>(d);
+    } else if (MODE == kEpiRLUpdate) {
       // solvers.hpp:290-291: x_next = x .* A^T(ratio); relative change terms.
-      NDC_EPI_LOOP(const float xn = in[c] * acc[c]; v = xn;
-                   if (ok) {
-                     const double d = static_cast<double>(xn) - static_cast<double>(in[c]);
-                     p0 += d * d;
-                     p1 += static_cast<double>(in[c]) * static_cast<double>(in[c]);
-                   })
-      break;
-    default:
-      NDC_EPI_LOOP((void)0)
-      break;
+      const float xn = in[c] * acc_c;
+      v = xn;
+      if (ok) {
+        const double d = static_cast<double>(xn) - static_cast<double>(in[c]);
+        p0 += d * d;
+        p1 += static_cast<double>(in[c]) * static_cast<double>(in[c]);
+      }
+    }
+    res[c] = (ok || MODE < 0) ? v : 0.f;
   }
-#undef NDC_EPI_LOOP
-  if (mode != kEpiKKT) {
+  return make_float4(res[0], res[1], res[2], res[3]);
+}
+
+template <int MODE>
+__host__ __device__ constexpr bool mode_reads_aux() {
+  return MODE == kEpiResid || MODE == kEpiPG || MODE == kEpiKKT || MODE == kEpiRLRatio || MODE == kEpiRLUpdate;
+}
+
+// Warp-collective coalesced load of the strip's 32 rows x 16 columns into a staging
+// buffer (lanes 4r..4r+3 read row r: 8 whole 64-byte segments per instruction instead of
+// 32 half sectors); the epilogue then reads lane-per-row from shared memory.
+template <class RowOk, class RowOff>
+__device__ __forceinline__ void load_rows(float* wst, int lane, const float* src, RowOk row_ok, RowOff row_off) {
 #pragma unroll
-    for (int q = 0; q < kRX / 4; ++q)
-      *reinterpret_cast<float4*>(a.out + o + 4 * q) =
-          make_float4(res[4 * q], res[4 * q + 1], res[4 * q + 2], res[4 * q + 3]);
+  for (int k = 0; k < 4; ++k) {
+    const int r = 8 * k + (lane >> 2), q = lane & 3;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row_ok(r)) x = *reinterpret_cast<const float4*>(src + row_off(r) + 4 * q);
+    *reinterpret_cast<float4*>(wst + stage_pos(r, q)) = x;
   }
-  if (mode == kEpiPG || mode == kEpiRLRatio) {
+}
+
+// Warp-collective store of the 32 staged rows x 16 columns (row r written by lane r):
+// every store instruction covers 8 whole 64-byte row segments (lanes 4r..4r+3 -> row r),
+// so each 32-byte sector is written completely by one instruction.  (A lane-per-row
+// store writes half sectors, which the L2 fills from DRAM first: measured ~2x DRAM
+// traffic on small PSFs.)  row_ok(r) / row_off(r): validity and buffer offset of row r.
+template <class RowOk, class RowOff>
+__device__ __forceinline__ void store_rows(const float* wst, int lane, float* dst, RowOk row_ok, RowOff row_off) {
 #pragma unroll
-    for (int q = 0; q < kRX / 4; ++q)
-      *reinterpret_cast<float4*>(a.aux_out + o + 4 * q) =
-          make_float4(aux[4 * q], aux[4 * q + 1], aux[4 * q + 2], aux[4 * q + 3]);
+  for (int k = 0; k < 4; ++k) {
+    const int r = 8 * k + (lane >> 2), q = lane & 3;
+    const float4 x = *reinterpret_cast<const float4*>(wst + stage_pos(r, q));
+    if (row_ok(r)) *reinterpret_cast<float4*>(dst + row_off(r) + 4 * q) = x;
+  }
+}
+
+// The epilogue of one warp's strip (16 columns x 32*RY rows) for epilogue mode MODE:
+// per 32-row block, staged coalesced loads (accum_in, aux_in), lane-per-row math,
+// staged coalesced stores (out, then aux_out) through the warp's own 2 KB buffer.
+//
+// STAGED = false (large PSFs, compute-bound): lane-per-row float4 loads / stores straight
+// to global memory -- no shuffle through shared memory and no warp syncs, so a warp's
+// epilogue overlaps its neighbours' FFMA work (the staged form measured 2-3 % slower on
+// config 2, the direct form ~30 % slower on 3x3 / 5x5 PSFs).
+template <int MODE, int RY, bool STAGED>
+__device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs& a, int b, int oz, int ox0,
+                                              int wrow0, int lane, float (&acc)[RY][kRX], float* wst, double& p0,
+                                              double& p1) {
+  constexpr bool kReadsAux = mode_reads_aux<MODE>();
+  constexpr bool kStoreOut = MODE != kEpiKKT;
+  constexpr bool kStoreAux = MODE == kEpiPG || MODE == kEpiRLRatio;
+  const long long obase = static_cast<long long>(b) * g.out_image +
+                          static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
+  const bool strip_ok = ox0 < g.out_ex;
+  const int cols_left = g.out_ex - ox0;
+  const float sc = (MODE >= 0 && a.scale != nullptr) ? a.scale[b] : 1.0f;
+  const float step = MODE == kEpiPG ? static_cast<float>(a.step[b]) : 0.f;
+#pragma unroll
+  for (int j = 0; j < RY; ++j) {
+    const int row0 = wrow0 + 32 * j;  // the warp's first row of block j
+    const bool mine = row0 + lane < g.out_ey && strip_ok;
+    auto row_ok = [&](int r) { return strip_ok && row0 + r < g.out_ey; };
+    auto row_off = [&](int r) { return obase + static_cast<long long>(row0 + r) * g.out_pitch; };
+    float* acc_j = acc[j];
+    if (!STAGED) {
+      const long long o = obase + static_cast<long long>(row0 + lane) * g.out_pitch;
+      if (!mine) continue;
+      float in[kRX];
+#pragma unroll
+      for (int q = 0; q < kRX / 4; ++q) {
+        if (g.accum) {
+          const float4 p = *reinterpret_cast<const float4*>(a.accum_in + o + 4 * q);
+          acc_j[4 * q] += p.x;
+          acc_j[4 * q + 1] += p.y;
+          acc_j[4 * q + 2] += p.z;
+          acc_j[4 * q + 3] += p.w;
+        }
+        if (kReadsAux) {
+          const float4 v = *reinterpret_cast<const float4*>(a.aux_in + o + 4 * q);
+          in[4 * q] = v.x;
+          in[4 * q + 1] = v.y;
+          in[4 * q + 2] = v.z;
+          in[4 * q + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kRX / 4; ++q) {
+        const float4 r = epilogue_res<MODE>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
+        if (kStoreOut) *reinterpret_cast<float4*>(a.out + o + 4 * q) = r;
+        if (kStoreAux) {
+          float x[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float v = MODE == kEpiPG ? acc_j[4 * q + c] : acc_j[4 * q + c] * sc - in[4 * q + c];
+            x[c] = 4 * q + c < cols_left ? v : 0.f;
+          }
+          *reinterpret_cast<float4*>(a.aux_out + o + 4 * q) = make_float4(x[0], x[1], x[2], x[3]);
+        }
+      }
+      continue;
+    }
+    if (g.accum) {  // partial sums of the earlier tap chunks
+      load_rows(wst, lane, a.accum_in, row_ok, row_off);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kRX / 4; ++q) {
+        const float4 p = *reinterpret_cast<const float4*>(wst + stage_pos(lane, q));
+        acc_j[4 * q] += p.x;
+        acc_j[4 * q + 1] += p.y;
+        acc_j[4 * q + 2] += p.z;
+        acc_j[4 * q + 3] += p.w;
+      }
+      __syncwarp();
+    }
+    if (kReadsAux) {
+      load_rows(wst, lane, a.aux_in, row_ok, row_off);
+      __syncwarp();
+    }
+    float in[kRX];
+#pragma unroll
+    for (int q = 0; q < kRX / 4; ++q) {
+      const int sp = stage_pos(lane, q);
+      if (kReadsAux) {
+        const float4 v = *reinterpret_cast<const float4*>(wst + sp);
+        in[4 * q] = v.x;
+        in[4 * q + 1] = v.y;
+        in[4 * q + 2] = v.z;
+        in[4 * q + 3] = v.w;
+      }
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (mine) r = epilogue_res<MODE>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
+      if (kStoreOut) *reinterpret_cast<float4*>(wst + sp) = r;  // same lane, same slot
+    }
+    if (kStoreOut) {
+      __syncwarp();
+      store_rows(wst, lane, a.out, row_ok, row_off);
+      __syncwarp();
+    }
+    if (kStoreAux) {  // kEpiPG: g = acc; kEpiRLRatio: A x - Y
+#pragma unroll
+      for (int q = 0; q < kRX / 4; ++q) {
+        float r[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float v = MODE == kEpiPG ? acc_j[4 * q + c] : acc_j[4 * q + c] * sc - in[4 * q + c];
+          r[c] = 4 * q + c < cols_left ? v : 0.f;
+        }
+        *reinterpret_cast<float4*>(wst + stage_pos(lane, q)) = make_float4(r[0], r[1], r[2], r[3]);
+      }
+      __syncwarp();
+      store_rows(wst, lane, a.aux_out, row_ok, row_off);
+      __syncwarp();
+    }
   }
 }
 
@@ -240,8 +354,22 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
 #ifndef NDC_MIN_BLOCKS
 #define NDC_MIN_BLOCKS 2
 #endif
+#ifndef NDC_SMALL_MIN_BLOCKS
+#define NDC_SMALL_MIN_BLOCKS 3
+#endif
+#ifndef NDC_STAGED_KX
+#define NDC_STAGED_KX 9  // staged (coalesced) epilogue up to this kernel x-extent
+#endif
+#ifndef NDC_SMALL_KX
+#define NDC_SMALL_KX 5
+#endif
+// Small kernels (KX <= NDC_SMALL_KX) are HBM-bound: more resident CTAs per SM keep more
+// tile loads in flight.
+template <int KX>
+constexpr int min_blocks_for() { return KX <= NDC_SMALL_KX ? NDC_SMALL_MIN_BLOCKS : NDC_MIN_BLOCKS; }
+
 template <int KX, int SH, int RY>
-__global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     correlate_kernel(const __grid_constant__ CUtensorMap map, const CorrGeom g, const CorrArgs a,
                      const __grid_constant__ TapBlock taps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -268,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
   const int n = kzB - kzA;
 
   const int sbytes = stage_bytes_aligned(g.rows, g.pitch_s);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + g.stages * sbytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + barrier_offset(g.stages, sbytes));
   const uint32_t tx_bytes = static_cast<uint32_t>(g.rows * g.pitch_s * 4);
 
   if (tid == 0) {
@@ -335,19 +463,23 @@ __global__ void __launch_bounds__(kThreads, NDC_MIN_BLOCKS)
     }
   }
 
-  // ---- epilogue --------------------------------------------------------------------
-  const int ox0 = tx0 + wx * kRX;
+  // ---- epilogue (one instantiation per mode: the dispatch happens once per tile) --------
+  float* wst = reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
   double p0 = 0.0, p1 = 0.0;
-#pragma unroll
-  for (int j = 0; j < RY; ++j) {
-    const int oy = ty0 + row_l + 32 * j;
-    if (oy < g.out_ey && ox0 < g.out_ex) {
-      const long long o = static_cast<long long>(b) * g.out_image +
-                          static_cast<long long>(g.out_z0 + oz) * g.out_plane +
-                          static_cast<long long>(oy) * g.out_pitch + ox0;
-      epilogue_strip(g, a, b, o, ox0, acc[j], p0, p1);
-    }
+#define NDC_EPI(M) \
+  epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, wst, p0, p1)
+  switch (g.final_chunk ? g.mode : -1) {
+    case kEpiStore: NDC_EPI(kEpiStore); break;
+    case kEpiResid: NDC_EPI(kEpiResid); break;
+    case kEpiNorm: NDC_EPI(kEpiNorm); break;
+    case kEpiPG: NDC_EPI(kEpiPG); break;
+    case kEpiKKT: NDC_EPI(kEpiKKT); break;
+    case kEpiClamp: NDC_EPI(kEpiClamp); break;
+    case kEpiRLRatio: NDC_EPI(kEpiRLRatio); break;
+    case kEpiRLUpdate: NDC_EPI(kEpiRLUpdate); break;
+    default: NDC_EPI(-1); break;
   }
+#undef NDC_EPI
 
   if (a.partials != nullptr) {
     // one partial per warp, written without a CTA barrier (finalize reduces them in a

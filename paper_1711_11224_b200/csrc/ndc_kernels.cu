@@ -266,7 +266,8 @@ int shared_pitch_for(int kx, int sh) {
 }
 
 size_t correlate_smem_bytes(const CorrGeom& g) {
-  return static_cast<size_t>(g.stages) * corr::stage_bytes_aligned(g.rows, g.pitch_s) +
+  // stage 0 doubles as the epilogue's per-warp staging buffers
+  return static_cast<size_t>(corr::barrier_offset(g.stages, corr::stage_bytes_aligned(g.rows, g.pitch_s))) +
          static_cast<size_t>(kMaxStages) * 8;
 }
 

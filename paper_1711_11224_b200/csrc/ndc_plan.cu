@@ -114,6 +114,7 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= 90 * 1024)) ? 2 : 1;
   }
   if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
+
   if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
 
   h64_.assign(h, h + count);
@@ -147,7 +148,15 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     xlo_ = 0;
     xhi_ = mz_;
   }
-  X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, 4) * 4));
+  // c0: >= 2p_x and a multiple of NDC_X_ALIGN floats (default 32 = one 128-byte line), so
+  // x-shaped output tiles cover whole lines and share none with their neighbours (a
+  // line written partly by two CTAs at different times costs DRAM read-modify-writes:
+  // measured ~2x write traffic on small PSFs at 16-byte alignment)
+  {
+    long long al = 32;
+    if (const char* e = std::getenv("NDC_X_ALIGN")) al = std::max(4LL, std::atoll(e) / 4 * 4);
+    X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, al) * al));
+  }
   Y_ = Vol::make(rhi_ - rlo_, my_ + 2 * py_, mx_ + 2 * px_);
 
   int ndev = 0;
