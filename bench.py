@@ -172,7 +172,11 @@ WORK = {
     "c3": dict(e2e_iters=50, steps=20, step=None, desc="3D 256x256x128, PSF 15x15x31 sigma_xy 1.5 sigma_z 4"),
     "c4": dict(e2e_iters=4, steps=5, step=1.0, desc="3D 1024x1024x512, PSF 9x9x21, Poisson 500"),
     "c5": dict(e2e_iters=2, steps=2, step=1.0, desc="3D 2048x2048x256, 33x33x65 3-Gaussian PSF, Poisson 200"),
+    # HBM-bound small-PSF case (not a BASELINE config; north_star's ">= 70 % HBM" target)
+    "c2s": dict(e2e_iters=100, steps=500, step=None,
+                desc="16x2048x2048 2D batch, PSF 5x5 sigma 1 (reference acceptance PSF), Poisson 1000"),
 }
+HBM_BOUND = ("c2s",)
 
 
 def inputs(config: str, rank: int, sharded: bool):
@@ -202,8 +206,8 @@ class RefRunner:
         self.orc = Oracle("ref" if self.kind == "reference" else "c")
         self.cores = os.cpu_count() or 1
         self.orc.set_threads(self.cores)
-        if config == "c2":
-            _, y, h = synth.make("c2", batch=1)
+        if config in ("c2", "c2s"):
+            _, y, h = synth.make(config, batch=1)
             self.y, self.h, self.xs = y[0], h, (2048, 2048)
         elif config == "c1":
             x, self.y, self.h = synth.make("c1")
@@ -212,7 +216,7 @@ class RefRunner:
             shape = {"c3": (128, 256, 256), "c4": (64, 128, 128), "c5": (64, 96, 96)}[config]
             x, self.y, self.h = synth.make(config, shape=shape, n_objects=200)
             self.xs = x.shape
-        self.sample = f"{'1 image' if config in ('c1', 'c2') else 'volume'} {self.xs}, PSF {self.h.shape}"
+        self.sample = f"{'1 image' if config in ('c1', 'c2', 'c2s') else 'volume'} {self.xs}, PSF {self.h.shape}"
         self.voxels = int(np.prod(self.xs))
         self.step0 = 1.0  # unit-sum PSFs: ||A|| <= 1; loop-body cost does not depend on it
 
@@ -242,6 +246,17 @@ def cpu_reference_sample(config: str, iters: int):
 
 
 # --- our arm ------------------------------------------------------------------------------------
+
+def measured_hbm_peak():
+    """(GB/s, basis): MEASURED_PEAKS.json's driver-measured copy bandwidth, else the
+    profiling guide's B200 fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["hbm_gbs"])
+        return v, f"MEASURED_PEAKS.json hbm_gbs (torch copy, read+write bytes): {v:.1f} GB/s"
+    except (OSError, ValueError, KeyError):
+        return 7700.0, "fallback: B200 HBM3e nominal 7.7 TB/s (MEASURED_PEAKS.json absent)"
+
 
 def make_plan(nd, d, x_shape, h, B, local, sharded):
     if not sharded:
@@ -319,6 +334,12 @@ def run_ours(a):
     achieved = flops_pass / avg_s / 1e12
     smax = clk.get("sm_max_mhz") or 1965.0
     peak = N_SM * FFMA_PER_SM_CLK * 2 * smax * 1e6 / 1e12
+    if a.config in HBM_BOUND:
+        # algorithmic bytes per pass (float32): forward reads x and Y, writes r; adjoint
+        # reads r and x, writes trial and g (Plan PG passes)
+        ny_rank = B * int(np.prod([s + k - 1 for s, k in zip(x_shape, h.shape)]))
+        bytes_pass = 4.0 * ((ny_rank + 3 * vox_rank) if dom == "adjoint" else (vox_rank + 2 * ny_rank))
+        hbm_peak = measured_hbm_peak()
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -339,7 +360,14 @@ def run_ours(a):
                    "tol_rel_objective": 0.0,
                    "step_size": "auto (power iteration, untimed setup)" if work["step"] is None
                    else f"initial_step={work['step']} (unit-sum PSF)"},
-        "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak,
+        "roofline": ({"bound": "hbm", "kernel": dom, "achieved": bytes_pass / avg_s / 1e9, "peak": hbm_peak[0],
+                      "unit": "GB/s", "frac": bytes_pass / avg_s / 1e9 / hbm_peak[0], "traffic": traffic,
+                      "peak_basis": hbm_peak[1], "algorithmic_bytes_per_pass": bytes_pass,
+                      "pass_ms": avg_s * 1e3, "launches_per_pass": n_dom / max(passes, 1),
+                      "fp32_tflops": achieved,
+                      "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}}
+                     if a.config in HBM_BOUND else
+                     {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_basis": f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (sm max clock); "
                                    "no measured FP32 peak in MEASURED_PEAKS.json",
@@ -347,7 +375,7 @@ def run_ours(a):
                      "launches_per_pass": n_dom / max(passes, 1),
                      "frac_at_observed_clock": (achieved / (N_SM * FFMA_PER_SM_CLK * 2 * clk["sm_mhz"] * 1e6 / 1e12)
                                                 if clk.get("sm_mhz") else None),
-                     "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}},
+                     "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}}),
         "gpu_launches": int(n_all),
         "clocks": clk,
         "iterations_accepted": int(rep.iterations_run),

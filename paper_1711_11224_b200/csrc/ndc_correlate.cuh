@@ -59,6 +59,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 16-byte global -> shared copy that bypasses the registers (and L1), tracked as a group.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -157,6 +164,10 @@ __device__ __forceinline__ float4 epilogue_res(int cols_left, const float* acc4,
   return make_float4(res[0], res[1], res[2], res[3]);
 }
 
+__host__ __device__ constexpr bool mode_reads_aux_rt(int m) {
+  return m == kEpiResid || m == kEpiPG || m == kEpiKKT || m == kEpiRLRatio || m == kEpiRLUpdate;
+}
+
 template <int MODE>
 __host__ __device__ constexpr bool mode_reads_aux() {
   return MODE == kEpiResid || MODE == kEpiPG || MODE == kEpiKKT || MODE == kEpiRLRatio || MODE == kEpiRLUpdate;
@@ -201,8 +212,8 @@ __device__ __forceinline__ void store_rows(const float* wst, int lane, float* ds
 // config 2, the direct form ~30 % slower on 3x3 / 5x5 PSFs).
 template <int MODE, int RY, bool STAGED>
 __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs& a, int b, int oz, int ox0,
-                                              int wrow0, int lane, float (&acc)[RY][kRX], float* wst, double& p0,
-                                              double& p1) {
+                                              int wrow0, int lane, float (&acc)[RY][kRX], float* wst,
+                                              const float* wpre, double& p0, double& p1) {
   constexpr bool kReadsAux = mode_reads_aux<MODE>();
   constexpr bool kStoreOut = MODE != kEpiKKT;
   constexpr bool kStoreAux = MODE == kEpiPG || MODE == kEpiRLRatio;
@@ -269,8 +280,14 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
       }
       __syncwarp();
     }
+    // aux_in: prefetched into wpre at kernel start (cp.async), else a staged load now
+    const float* src_in = wpre != nullptr ? wpre + j * (32 * kRX) : wst;
     if (kReadsAux) {
-      load_rows(wst, lane, a.aux_in, row_ok, row_off);
+      if (wpre != nullptr) {
+        if (j == 0) cp_async_wait_all();
+      } else {
+        load_rows(wst, lane, a.aux_in, row_ok, row_off);
+      }
       __syncwarp();
     }
     float in[kRX];
@@ -278,7 +295,7 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
     for (int q = 0; q < kRX / 4; ++q) {
       const int sp = stage_pos(lane, q);
       if (kReadsAux) {
-        const float4 v = *reinterpret_cast<const float4*>(wst + sp);
+        const float4 v = *reinterpret_cast<const float4*>(src_in + sp);
         in[4 * q] = v.x;
         in[4 * q + 1] = v.y;
         in[4 * q + 2] = v.z;
@@ -355,13 +372,13 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
 #define NDC_MIN_BLOCKS 2
 #endif
 #ifndef NDC_SMALL_MIN_BLOCKS
-#define NDC_SMALL_MIN_BLOCKS 3
+#define NDC_SMALL_MIN_BLOCKS 4
 #endif
 #ifndef NDC_STAGED_KX
-#define NDC_STAGED_KX 9  // staged (coalesced) epilogue up to this kernel x-extent
+#define NDC_STAGED_KX kStagedMaxKX  // staged (coalesced) epilogue up to this kernel x-extent
 #endif
 #ifndef NDC_SMALL_KX
-#define NDC_SMALL_KX 5
+#define NDC_SMALL_KX kSmallMaxKX
 #endif
 // Small kernels (KX <= NDC_SMALL_KX) are HBM-bound: more resident CTAs per SM keep more
 // tile loads in flight.
@@ -413,6 +430,31 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
       tma_load_3d(smem_raw + i * sbytes, &map, &bars[i], tx0 + g.off_x, ty0 + g.off_y,
                   b * g.in_ez + iz);
     }
+  }
+
+  // Small PSFs: prefetch the epilogue's aux_in strip (Y or x) into shared memory now,
+  // so it arrives during the FFMA loop instead of stalling the epilogue.
+  const float* wpre = nullptr;
+  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode)) {
+    float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
+                 warp * (RY * 32 * kRX);
+    const int ox0 = tx0 + wx * kRX;
+    const long long obase = static_cast<long long>(b) * g.out_image +
+                            static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
+    if (ox0 < g.out_ex) {
+#pragma unroll
+      for (int j = 0; j < RY; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = 8 * k + (lane >> 2), q = lane & 3;
+          const int row = ty0 + wy * (32 * RY) + 32 * j + r;
+          if (row < g.out_ey)
+            cp_async16(pre + j * (32 * kRX) + stage_pos(r, q),
+                       a.aux_in + obase + static_cast<long long>(row) * g.out_pitch + 4 * q);
+        }
+    }
+    cp_async_commit();
+    wpre = pre;
   }
 
   float acc[RY][kRX];
@@ -467,7 +509,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   float* wst = reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
   double p0 = 0.0, p1 = 0.0;
 #define NDC_EPI(M) \
-  epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, wst, p0, p1)
+  epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, wst, \
+                                             wpre, p0, p1)
   switch (g.final_chunk ? g.mode : -1) {
     case kEpiStore: NDC_EPI(kEpiStore); break;
     case kEpiResid: NDC_EPI(kEpiResid); break;
@@ -499,7 +542,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
 template <int KX, int SH, int RY>
 cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs& a,
                       const TapBlock& taps, int batch, int nz_out, cudaStream_t s) {
-  const size_t smem = correlate_smem_bytes(g);
+  // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
+  const size_t smem = correlate_smem_bytes(g) +
+                      ((KX <= NDC_STAGED_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY>,

@@ -28,6 +28,11 @@ constexpr int kMaxKX = 33;        // largest x-extent with a register-window ins
 constexpr int kMaxRows = 256;     // TMA box limit on rows: kTileY + KY - 1 <= 256
 constexpr int kTapCap = 7680;     // taps per launch carried in the kernel parameter block
 constexpr int kMaxStages = 3;
+// HBM-bound small PSFs (ndc_correlate.cuh): kernel x-extents up to kStagedMaxKX use the
+// staged, sector-complete epilogue (and, for single-plane problems, a cp.async prefetch
+// of the epilogue's aux_in strip); up to kSmallMaxKX also 64-row tiles at 4 CTAs / SM.
+constexpr int kStagedMaxKX = 9;
+constexpr int kSmallMaxKX = 5;
 
 // Epilogue selector (uniform per launch).
 enum EpiMode : int {
@@ -59,6 +64,7 @@ struct CorrGeom {
   int tiles_x, tiles_y;
   int rows, pitch_s;   // shared tile: rows x pitch_s floats per stage
   int stages;
+  int aux_prefetch;    // cp.async the epilogue's aux_in strip at kernel start (small PSFs)
   int accum;           // add the partial sum held in `accum_in`
   int mode;            // EpiMode (ignored unless final)
   int final_chunk;     // last tap chunk: apply the epilogue

@@ -112,6 +112,8 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     const long long stage2 = static_cast<long long>(2 * kTileY + KY_ - 1) * pitch2 * 4;
     const bool fits = 2 * kTileY + KY_ - 1 <= kMaxRows;
     ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= 90 * 1024)) ? 2 : 1;
+    // small PSFs are HBM-bound: 64-row tiles at 4 CTAs / SM keep more loads in flight
+    if (KX_ <= kSmallMaxKX) ry_ = 1;
   }
   if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
 
@@ -507,6 +509,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     g.kz0 = c * slices_per;
     g.kz1 = std::min(KZ_, g.kz0 + slices_per);
     g.stages = std::min(stages_, g.kz1 - g.kz0);
+    g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
     g.accum = c > 0;
     g.final_chunk = (c == nchunks - 1);
     // x-shaped operands are addressed from their interior origin
