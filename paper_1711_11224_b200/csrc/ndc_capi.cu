@@ -262,6 +262,8 @@ ndc_status ndc_deconv_pg_batch_f64(size_t batch, int ndim, const size_t* y_ext, 
     if ((obj_trace || kkt_trace) && trace_cap < c.max_iters + 1)
       ndc::fail(NDC_ERR_ARGUMENT, "trace_cap must be at least max_iters + 1");
     auto p = one_shot(batch, ndim, x_ext, k_ext, h);
+    if (!c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
+      p->estimate_launch(c.power_iters);  // overlaps the upload below
     p->set_observation_f64(y);
     p->pg_begin(c);
     p->pg_iterate(c.max_iters);
@@ -289,6 +291,8 @@ ndc_status ndc_deconv_pg_batch_f32(size_t batch, int ndim, const size_t* y_ext, 
     if ((obj_trace || kkt_trace) && trace_cap < c.max_iters + 1)
       ndc::fail(NDC_ERR_ARGUMENT, "trace_cap must be at least max_iters + 1");
     auto p = one_shot(batch, ndim, x_ext, k_ext, h);
+    if (!c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
+      p->estimate_launch(c.power_iters);  // overlaps the upload below
     p->set_observation_f32(y);
     p->pg_begin(c);
     p->pg_iterate(c.max_iters);

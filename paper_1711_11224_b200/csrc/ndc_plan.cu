@@ -23,6 +23,11 @@
 namespace ndc {
 
 namespace {
+void* small_pinned_get(size_t bytes);
+void small_pinned_put(size_t bytes, void* p);
+}  // namespace
+
+namespace {
 // Device scalar slots (doubles), per image unless noted.
 enum Slot { kF = 0, kKKT = 1, kCHG = 2, kAUX = 3, kNumSlots = 4 };
 constexpr int kMaxPowerIters = 4096;
@@ -191,7 +196,8 @@ Plan::~Plan() {
                   staging_})
     if (p) cudaFreeAsync(p, stream_);
   if (stream_) cudaStreamSynchronize(stream_);
-  delete[] hsc_;
+  if (hsc_) small_pinned_put(small_bytes_, hsc_);
+  if (up_ev_) cudaEventDestroy(up_ev_);
   release_pinned();
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -316,6 +322,28 @@ struct PinnedRing {
 };
 std::mutex g_ring_mu;
 std::vector<PinnedRing> g_rings;
+
+// Small pinned blocks (per-plan scalar mirrors), cached per process by size.
+std::mutex g_small_mu;
+std::vector<std::pair<size_t, void*>> g_small;
+void* small_pinned_get(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_small_mu);
+    for (size_t i = 0; i < g_small.size(); ++i)
+      if (g_small[i].first == bytes) {
+        void* p = g_small[i].second;
+        g_small.erase(g_small.begin() + static_cast<long>(i));
+        return p;
+      }
+  }
+  void* p = nullptr;
+  check_cuda(cudaMallocHost(&p, bytes), "cudaMallocHost scalars");
+  return p;
+}
+void small_pinned_put(size_t bytes, void* p) {
+  std::lock_guard<std::mutex> lk(g_small_mu);
+  g_small.emplace_back(bytes, p);
+}
 }  // namespace
 
 void Plan::ensure_pinned() {
@@ -426,7 +454,12 @@ void Plan::alloc_all() {
   const size_t nsc = kNumSlots * B_ + kMaxPowerIters + 16;
   dsc_ = static_cast<double*>(dmalloc(nsc * sizeof(double)));
   check_cuda(cudaMemsetAsync(dsc_, 0, nsc * sizeof(double), stream_), "cudaMemset");
-  hsc_ = new double[nsc]();  // small scalar mirror (pageable: no cudaFreeHost on destroy)
+  // pinned scalar mirrors: [nsc doubles of D2H results][B steps][B active flags]
+  small_bytes_ = ((nsc + B_) * sizeof(double) + B_ * sizeof(int) + 4095) / 4096 * 4096;
+  hsc_ = static_cast<double*>(small_pinned_get(small_bytes_));
+  hstep_ = hsc_ + nsc;
+  hact_ = reinterpret_cast<int*>(hstep_ + B_);
+  check_cuda(cudaEventCreateWithFlags(&up_ev_, cudaEventDisableTiming), "cudaEventCreate");
   dscale_ = static_cast<float*>(dmalloc(B_ * sizeof(float)));
   dactive_ = static_cast<int*>(dmalloc(B_ * sizeof(int)));
   dstep_ = static_cast<double*>(dmalloc(B_ * sizeof(double)));
@@ -435,6 +468,7 @@ void Plan::alloc_all() {
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   std::vector<int> act(B_, 1);
   check_cuda(cudaMemcpyAsync(dactive_, act.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+  act_cache_ = act;
   staging_bytes_ = static_cast<size_t>(std::max(X_.ez * static_cast<long long>(X_.ey) * X_.ex,
                                                 Y_.ez * static_cast<long long>(Y_.ey) * Y_.ex)) * 8;
   staging_ = dmalloc(staging_bytes_);
@@ -612,22 +646,104 @@ void Plan::halo_y(float* buf) {
                   hi ? at(xb_ + pz_) : nullptr, n, stream_);
 }
 
+// Per-image flags / steps go to the device only when they change (they rarely do), from
+// pinned mirrors, without a stream sync; up_ev_ guards the mirror against reuse while
+// an earlier upload is still in flight.
 void Plan::upload_active(const std::vector<int>& act) {
-  check_cuda(cudaMemcpyAsync(dactive_, act.data(), act.size() * sizeof(int), cudaMemcpyHostToDevice,
-                             stream_),
+  if (act == act_cache_) return;
+  check_cuda(cudaEventSynchronize(up_ev_), "cudaEventSynchronize");
+  std::memcpy(hact_, act.data(), act.size() * sizeof(int));
+  check_cuda(cudaMemcpyAsync(dactive_, hact_, act.size() * sizeof(int), cudaMemcpyHostToDevice, stream_),
              "H2D active");
-  sync();  // act lives on the host stack of the caller
+  check_cuda(cudaEventRecord(up_ev_, stream_), "cudaEventRecord");
+  act_cache_ = act;
+}
+
+void Plan::upload_steps(const std::vector<double>& steps) {
+  if (steps == step_cache_) return;
+  check_cuda(cudaEventSynchronize(up_ev_), "cudaEventSynchronize");
+  std::memcpy(hstep_, steps.data(), steps.size() * sizeof(double));
+  check_cuda(cudaMemcpyAsync(dstep_, hstep_, steps.size() * sizeof(double), cudaMemcpyHostToDevice, stream_),
+             "H2D steps");
+  check_cuda(cudaEventRecord(up_ev_, stream_), "cudaEventRecord");
+  step_cache_ = steps;
 }
 
 // ---- host <-> device packing (dense row-major host, pitched device) -----------------
+namespace {
+// dst[i] = float(src[i]) / double(src[i]) over the host pool (round to nearest: the same
+// value the device conversion would give).
+template <class D, class S>
+void par_convert(D* dst, const S* src, size_t n) {
+  const unsigned parts = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(HostPool::get().width(), n >> 18)));
+  HostPool::get().run(parts, [&](unsigned i) {
+    const auto r = part_range(n, parts, i);
+    for (size_t k = r.first; k < r.second; ++k) dst[k] = static_cast<D>(src[k]);
+  });
+}
+}  // namespace
+
+// f64 host -> f32 device: host threads convert into the pinned ring (half the PCIe
+// bytes of shipping f64 and converting on the device; identical values).
+void Plan::h2d_f64_as_f32(float* dev, const double* host, size_t n) {
+  ensure_pinned();
+  const size_t chunk = kPinChunk / 4;
+  size_t i = 0;
+  for (size_t off = 0; off < n; off += chunk, ++i) {
+    const int s = static_cast<int>(i & 1);
+    const size_t m = std::min(chunk, n - off);
+    if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    par_convert(static_cast<float*>(hpin_[s]), host + off, m);
+    check_cuda(cudaMemcpyAsync(dev + off, hpin_[s], m * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
+  }
+}
+
+// f32 device -> f64 host: the DMA of chunk i+1 overlaps the host conversion of chunk i.
+void Plan::d2h_f32_as_f64(double* host, const float* dev, size_t n) {
+  ensure_pinned();
+  const size_t chunk = kPinChunk / 4;
+  const size_t nch = (n + chunk - 1) / chunk;
+  auto issue = [&](size_t i) {
+    const int s = static_cast<int>(i & 1);
+    const size_t off = i * chunk, m = std::min(chunk, n - off);
+    check_cuda(cudaMemcpyAsync(hpin_[s], dev + off, m * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
+  };
+  if (nch == 0) return;
+  issue(0);
+  for (size_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch) issue(i + 1);
+    const int s = static_cast<int>(i & 1);
+    check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    const size_t off = i * chunk, m = std::min(chunk, n - off);
+    par_convert(host + off, static_cast<const float*>(hpin_[s]), m);
+  }
+}
+
 void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  // f64 -> f32 on the host threads, then f32 over PCIe (measured 13.8 vs 15.7 ms for the
+  // config-2 batch against the f64 DMA + device conversion)
+  static const bool hostconv = [] {
+    const char* e = std::getenv("NDC_H2D_HOSTCONV");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const bool big = hostconv && per * 8 >= (size_t(4) << 20);
   for (size_t b = 0; b < B_; ++b) {
-    h2d_staged(staging_, host + b * per, per * 8);
-    check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
-                               dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
-                               v.geo(nz), stream_),
-               "pack");
+    if (big) {
+      h2d_f64_as_f32(static_cast<float*>(staging_), host + b * per, per);
+      check_cuda(launch_pack_f32(static_cast<const float*>(staging_),
+                                 dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
+                                 v.geo(nz), stream_),
+                 "pack");
+    } else {
+      h2d_staged(staging_, host + b * per, per * 8);
+      check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
+                                 dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane, 1,
+                                 v.geo(nz), stream_),
+                 "pack");
+    }
     st_[2].launches++;
   }
   sync();
@@ -648,12 +764,28 @@ void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off
 
 void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz) {
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
+  // Host-side f32 -> f64 conversion halves the PCIe bytes but measured slower than the
+  // device conversion + f64 DMA + parallel memcpy (31 vs 19 ms for 16 x 2048^2 on the
+  // 16-core box: the host conversion is bound by host memory bandwidth); off by default.
+  static const bool hostconv = [] {
+    const char* e = std::getenv("NDC_D2H_HOSTCONV");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  const bool big = hostconv && per * 8 >= (size_t(4) << 20);
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(launch_unpack_f64(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
-                                 static_cast<double*>(staging_), 1, v.geo(nz), stream_),
-               "unpack");
-    st_[2].launches++;
-    d2h_staged(host + b * per, staging_, per * 8);
+    if (big) {
+      check_cuda(launch_unpack_f32(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
+                                   static_cast<float*>(staging_), 1, v.geo(nz), stream_),
+                 "unpack");
+      st_[2].launches++;
+      d2h_f32_as_f64(host + b * per, static_cast<const float*>(staging_), per);
+    } else {
+      check_cuda(launch_unpack_f64(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
+                                   static_cast<double*>(staging_), 1, v.geo(nz), stream_),
+                 "unpack");
+      st_[2].launches++;
+      d2h_staged(host + b * per, staging_, per * 8);
+    }
   }
 }
 
@@ -727,16 +859,31 @@ double Plan::op_kkt_residual() {
 // next forward pass as an output scale read on the device, so the 2*iters passes run
 // without a host round trip.
 double Plan::estimate_step(size_t power_iters) {
+  if (estimate_pending_ == power_iters) return estimate_collect();
+  estimate_launch(power_iters);
+  return estimate_collect();
+}
+
+// The power iteration's passes and the read-back of every iterate's norm are only
+// enqueued here; estimate_collect() waits.  The one-shot C-ABI calls launch it before
+// they upload the observation (it needs only the PSF and the shape), so the host-side
+// conversion of Y overlaps these device passes.
+void Plan::estimate_launch(size_t power_iters) {
   if (power_iters == 0) fail(NDC_ERR_CONFIG, "estimate_step: power_iters must be positive");
   if (power_iters > static_cast<size_t>(kMaxPowerIters))
     fail(NDC_ERR_UNSUPPORTED, "estimate_step: power_iters too large");
   if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "estimate_step: degenerate all-zero kernel");
   const double n = static_cast<double>(mz_) * my_ * mx_;
+  estimate_pending_ = 0;
   // Small problems run the power iteration in float64: when all-ones is an exact but
   // non-dominant eigenvector of A^T A (symmetric tiny shapes), the reference's f64
   // iteration stays in that eigenspace and float32 rounding would not.
-  if (world_ == 1 && n * static_cast<double>(h64_.size()) <= static_cast<double>(1 << 28))
-    return estimate_step_f64(power_iters);
+  if (world_ == 1 && n * static_cast<double>(h64_.size()) <= static_cast<double>(1 << 28)) {
+    estimate_value_ = estimate_step_f64(power_iters);
+    estimate_pending_ = power_iters;
+    estimate_f64_ = true;
+    return;
+  }
   const size_t saveB = B_;
   // image 0 only: launch with batch 1 (buffers are laid out image-major)
   B_ = 1;
@@ -756,21 +903,32 @@ double Plan::estimate_step(size_t power_iters) {
       finalize(partials_per_image(kAdj), kFinNorm, lam + i, nullptr, dscale_, nullptr);
     }
     check_cuda(cudaMemcpyAsync(hsc_, lam, power_iters * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
-    sync();
   } catch (...) {
     B_ = saveB;
+    maps_.clear();
     throw;
   }
   B_ = saveB;
   maps_.clear();  // maps were encoded with zcount for batch 1
+  estimate_pending_ = power_iters;
+  estimate_f64_ = false;
+}
+
+double Plan::estimate_collect() {
+  const size_t power_iters = estimate_pending_;
+  if (power_iters == 0) fail(NDC_ERR_ARGUMENT, "estimate_collect without estimate_launch");
+  estimate_pending_ = 0;
+  if (estimate_f64_) return estimate_value_;
+  sync();
   for (size_t i = 0; i < power_iters; ++i)
     if (!(hsc_[i] > 0.0) || !std::isfinite(hsc_[i]))
       fail(NDC_ERR_NUMERIC, "estimate_step: degenerate convolution operator");
+  const double step = 1.0 / hsc_[power_iters - 1];
   // restore the per-image scale to 1 for later kEpiStore users
   std::vector<float> ones(B_, 1.0f);
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   sync();
-  return 1.0 / hsc_[power_iters - 1];
+  return step;
 }
 
 // ---- NDTENSOR streaming (imageio.hpp:24-125 format) ----------------------------------------
@@ -1040,7 +1198,7 @@ void Plan::pg_begin(const ndc_deconv_config& c) {
   finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kF * B_, nullptr, nullptr, nullptr);
   check_cuda(cudaMemcpyAsync(hsc_, dsc_ + kF * B_, B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
   std::vector<double> steps(B_, step0_);
-  check_cuda(cudaMemcpyAsync(dstep_, steps.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+  upload_steps(steps);
   sync();
   for (size_t b = 0; b < B_; ++b) {
     img_[b].f = hsc_[b];
@@ -1065,8 +1223,7 @@ size_t Plan::pg_iterate(size_t n) {
     }
     if (active_count == 0) break;
     upload_active(act);
-    std::vector<double> steps(B_, step0_);
-    check_cuda(cudaMemcpyAsync(dstep_, steps.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+    upload_steps(std::vector<double>(B_, step0_));
 
     // g = A^T(A x - y) with kkt, trial = max(x - step0 g, 0), changed count (180-191)
     correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, dactive_, true);
@@ -1114,7 +1271,7 @@ size_t Plan::pg_iterate(size_t n) {
       }
       if (nb == 0) break;
       upload_active(bt);
-      check_cuda(cudaMemcpyAsync(dstep_, stp.data(), B_ * 8, cudaMemcpyHostToDevice, stream_), "H2D");
+      upload_steps(stp);
       check_cuda(launch_pg_trial(x_owned(x_), x_owned(g_), x_owned(trial_), dstep_, dactive_, partials_,
                                  static_cast<int>(B_), X_.geo(xa_n_), kElemBlocks, stream_),
                  "pg_trial launch");

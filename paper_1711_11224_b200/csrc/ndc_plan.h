@@ -95,6 +95,9 @@ class Plan {
   void op_normal_gradient();           // g = A^T (A x - y)
   double op_kkt_residual();            // max|min(x, A^T(Ax - y))|
   double estimate_step(size_t power_iters);
+  void estimate_launch(size_t power_iters);  // enqueue only (see ndc_plan.cu)
+  bool kernel_all_zero() const { return kernel_all_zero_; }
+  double estimate_collect();
   double estimate_step_f64(size_t power_iters);  // small problems (reference-exact)
 
   // --- projected gradient (solvers.hpp:155-238) ---
@@ -143,6 +146,9 @@ class Plan {
   void copy_image_y(float* dst, const float* src, size_t b);
   void sync();
   void upload_active(const std::vector<int>& act);
+  void upload_steps(const std::vector<double>& steps);
+  void h2d_f64_as_f32(float* dev, const double* host, size_t n);
+  void d2h_f32_as_f64(double* host, const float* dev, size_t n);
   void pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz);
   void pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz);
   void unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz);
@@ -184,7 +190,16 @@ class Plan {
   int* dactive_ = nullptr;
   double* dstep_ = nullptr;
   double* gather_ = nullptr;
-  double* hsc_ = nullptr;   // pinned host mirror
+  double* hsc_ = nullptr;   // pinned host mirror of the device scalars
+  double* hstep_ = nullptr;  // pinned upload mirrors (same block)
+  int* hact_ = nullptr;
+  size_t small_bytes_ = 0;
+  cudaEvent_t up_ev_ = nullptr;
+  size_t estimate_pending_ = 0;  // power_iters of a launched, uncollected estimate
+  bool estimate_f64_ = false;
+  double estimate_value_ = 0.0;
+  std::vector<int> act_cache_;        // last uploaded per-image flags / steps
+  std::vector<double> step_cache_;
   void* staging_ = nullptr;
   size_t staging_bytes_ = 0;
   std::map<std::pair<const float*, int>, CUtensorMap> maps_;
