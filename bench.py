@@ -417,9 +417,12 @@ def e2e(a, nd, y32, h, x_shape, B, work, world, d):
         if rc:
             raise RuntimeError(N.lib().ndc_last_error().decode())
 
+    t0 = time.perf_counter()
     call()  # warm-up (module load, allocator)
+    first = time.perf_counter() - t0
     reps_t = []
-    for _ in range(2):
+    # best of 3 (2 for solves over 2 s): the host side of the transfers is noisy
+    for _ in range(3 if first < 2.0 else 2):
         d.barrier()
         t0 = time.perf_counter()
         call()

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/ndconv_b200.h).  Converts the reference's f64 dense
 // tensors at the edge, maps internal failures to ndc_status codes that correspond to
 // the reference's exception types, and keeps the message per thread.
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -67,6 +68,14 @@ void check_forward(int ndim, const size_t* y_ext, const size_t* k_ext, const siz
 std::unique_ptr<ndc::Plan> one_shot(size_t batch, int ndim, const size_t* x_ext, const size_t* k_ext,
                                     const double* h) {
   return std::make_unique<ndc::Plan>(g_device, batch, ndim, x_ext, k_ext, h);
+}
+
+bool early_estimate() {
+  static const bool on = [] {
+    const char* e = std::getenv("NDC_EARLY_ESTIMATE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
 }
 
 ndc_deconv_config default_cfg() {
@@ -262,7 +271,7 @@ ndc_status ndc_deconv_pg_batch_f64(size_t batch, int ndim, const size_t* y_ext, 
     if ((obj_trace || kkt_trace) && trace_cap < c.max_iters + 1)
       ndc::fail(NDC_ERR_ARGUMENT, "trace_cap must be at least max_iters + 1");
     auto p = one_shot(batch, ndim, x_ext, k_ext, h);
-    if (!c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
+    if (early_estimate() && !c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
       p->estimate_launch(c.power_iters);  // overlaps the upload below
     p->set_observation_f64(y);
     p->pg_begin(c);
@@ -291,7 +300,7 @@ ndc_status ndc_deconv_pg_batch_f32(size_t batch, int ndim, const size_t* y_ext, 
     if ((obj_trace || kkt_trace) && trace_cap < c.max_iters + 1)
       ndc::fail(NDC_ERR_ARGUMENT, "trace_cap must be at least max_iters + 1");
     auto p = one_shot(batch, ndim, x_ext, k_ext, h);
-    if (!c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
+    if (early_estimate() && !c.has_initial_step && c.power_iters > 0 && !p->kernel_all_zero())
       p->estimate_launch(c.power_iters);  // overlaps the upload below
     p->set_observation_f32(y);
     p->pg_begin(c);
