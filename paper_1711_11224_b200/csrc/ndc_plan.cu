@@ -189,6 +189,7 @@ Plan::~Plan() {
     cudaEventDestroy(e.second);
   }
   for (void* p : {static_cast<void*>(x_), static_cast<void*>(trial_), static_cast<void*>(g_),
+                  static_cast<void*>(trial2_), static_cast<void*>(g2_),
                   static_cast<void*>(yobs_), static_cast<void*>(r_), static_cast<void*>(rt_),
                   static_cast<void*>(scratch_), static_cast<void*>(partials_),
                   static_cast<void*>(dsc_), static_cast<void*>(dscale_),
@@ -198,6 +199,7 @@ Plan::~Plan() {
   if (stream_) cudaStreamSynchronize(stream_);
   if (hsc_) small_pinned_put(small_bytes_, hsc_);
   if (up_ev_) cudaEventDestroy(up_ev_);
+  if (d2h_ev_) cudaEventDestroy(d2h_ev_);
   release_pinned();
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -460,6 +462,7 @@ void Plan::alloc_all() {
   hstep_ = hsc_ + nsc;
   hact_ = reinterpret_cast<int*>(hstep_ + B_);
   check_cuda(cudaEventCreateWithFlags(&up_ev_, cudaEventDisableTiming), "cudaEventCreate");
+  check_cuda(cudaEventCreateWithFlags(&d2h_ev_, cudaEventDisableTiming), "cudaEventCreate");
   dscale_ = static_cast<float*>(dmalloc(B_ * sizeof(float)));
   dactive_ = static_cast<int*>(dmalloc(B_ * sizeof(int)));
   dstep_ = static_cast<double*>(dmalloc(B_ * sizeof(double)));
@@ -1206,11 +1209,24 @@ void Plan::pg_begin(const ndc_deconv_config& c) {
     img_[b].step = step0_;
   }
   halo_y(r_);
+  spec_ready_ = false;
   pg_begun_ = true;
 }
 
+// One PG iteration per step, per image (solvers.hpp:179-228).  Common case -- every
+// active image accepts its first trial -- runs speculatively ahead: right after the
+// forward pass and the scalar read-back of step k are enqueued, the adjoint of step k+1
+// is enqueued too (as if every trial is accepted: r = r_trial, x = trial, into spare
+// buffers), so the device keeps working while the host makes step k's decision.  When
+// every image did accept (and none stops), the buffers rotate and step k+1 starts at
+// its forward pass; otherwise the speculative pass is discarded (its inputs are
+// unchanged, so it is exact when kept).  One-GPU plans only.
 size_t Plan::pg_iterate(size_t n) {
   if (!pg_begun_) fail(NDC_ERR_ARGUMENT, "pg_iterate before pg_begin");
+  static const bool spec_on = [] {
+    const char* e = std::getenv("NDC_SPECULATE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
   size_t active_count = 0;
   for (size_t step = 0; step < n; ++step) {
     std::vector<int> act(B_, 0);
@@ -1222,19 +1238,38 @@ size_t Plan::pg_iterate(size_t n) {
       active_count += act[b];
     }
     if (active_count == 0) break;
+    if (spec_ready_ && act != act_cache_) spec_ready_ = false;  // the set changed: recompute
     upload_active(act);
     upload_steps(std::vector<double>(B_, step0_));
 
-    // g = A^T(A x - y) with kkt, trial = max(x - step0 g, 0), changed count (180-191)
-    correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, dactive_, true);
-    finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
-             dactive_);
+    if (!spec_ready_) {
+      // g = A^T(A x - y) with kkt, trial = max(x - step0 g, 0), changed count (180-191)
+      correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, dactive_, true);
+      finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
+               dactive_);
+    }
+    spec_ready_ = false;
     halo_x(trial_);
     // A trial, residual, f_trial (195-197)
     correlate(kFwd, trial_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, dactive_, true);
     finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kAUX * B_, nullptr, nullptr, dactive_);
     check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
-    sync();
+    check_cuda(cudaEventRecord(d2h_ev_, stream_), "cudaEventRecord");
+
+    // speculative adjoint of the next step (see above); needs a next step for every image
+    bool spec = spec_on && world_ == 1;
+    for (size_t b = 0; b < B_ && spec; ++b)
+      if (act[b] && img_[b].kkt.size() + 1 >= cfg_.max_iters) spec = false;
+    if (spec) {
+      if (!trial2_) {
+        const long long nx = X_.image * static_cast<long long>(B_);
+        trial2_ = dev_alloc_f(nx);
+        g2_ = dev_alloc_f(nx);
+      }
+      correlate(kAdj, rt_, trial2_, kEpiPG, g2_, trial_, nullptr, dstep_, dactive_, true);
+      finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr, dactive_);
+    }
+    check_cuda(cudaEventSynchronize(d2h_ev_), "cudaEventSynchronize");
 
     // per-image decision (191-205)
     enum { kAccept, kFixed, kBacktrack, kStall };
@@ -1253,6 +1288,9 @@ size_t Plan::pg_iterate(size_t n) {
       else
         state[b] = kBacktrack;
     }
+    bool all_accept = true;
+    for (size_t b = 0; b < B_; ++b)
+      if (act[b] && state[b] != kAccept) all_accept = false;
     // backtracking: step *= factor, up to max_backtracks more trials (189, 205)
     for (;;) {
       std::vector<int> bt(B_, 0);
@@ -1293,16 +1331,18 @@ size_t Plan::pg_iterate(size_t n) {
       }
     }
     // commit (208-227)
-    bool any_accept = false;
+    bool any_accept = false, any_stop = false;
     for (size_t b = 0; b < B_; ++b) {
       if (!act[b]) continue;
       Img& im = img_[b];
       if (state[b] == kFixed) {
         im.reason = NDC_STOP_CONVERGED;
         im.active = false;
+        any_stop = true;
       } else if (state[b] == kStall) {
         im.reason = NDC_STOP_STALLED;
         im.active = false;
+        any_stop = true;
       } else {
         any_accept = true;
         const double drop = im.f - ft[b];
@@ -1312,8 +1352,21 @@ size_t Plan::pg_iterate(size_t n) {
         if (drop <= cfg_.tol_rel_objective * im.obj[im.obj.size() - 2]) {
           im.reason = NDC_STOP_CONVERGED;
           im.active = false;
+          any_stop = true;
         }
       }
+    }
+    if (spec && all_accept && !any_stop) {
+      // keep the speculative adjoint: x <- trial, r <- r_trial, and the next step's
+      // trial / g are already in trial2 / g2
+      float* old_x = x_;
+      x_ = trial_;
+      trial_ = trial2_;
+      trial2_ = old_x;
+      std::swap(g_, g2_);
+      std::swap(r_, rt_);
+      spec_ready_ = true;
+      continue;
     }
     if (any_accept) {
       std::swap(x_, trial_);
@@ -1346,6 +1399,7 @@ void Plan::copy_image_y(float* dst, const float* src, size_t b) {
 
 void Plan::pg_end() {
   if (!pg_begun_) fail(NDC_ERR_ARGUMENT, "pg_end before pg_begin");
+  spec_ready_ = false;  // a speculative next-step adjoint, if any, is simply dropped
   // solvers.hpp:230-233: one more adjoint for images whose last iterate has no KKT.
   std::vector<int> need(B_, 0);
   size_t nneed = 0;

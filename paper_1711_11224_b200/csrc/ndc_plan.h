@@ -182,6 +182,9 @@ class Plan {
 
   // device buffers
   float *x_ = nullptr, *trial_ = nullptr, *g_ = nullptr;
+  float *trial2_ = nullptr, *g2_ = nullptr;  // speculative next-step adjoint outputs
+  bool spec_ready_ = false;                  // this step's adjoint already ran speculatively
+  cudaEvent_t d2h_ev_ = nullptr;
   float *yobs_ = nullptr, *r_ = nullptr, *rt_ = nullptr, *scratch_ = nullptr;
   double2* partials_ = nullptr;
   long long partials_cap_ = 0;
