@@ -5,10 +5,14 @@ after the full iteration count; objective / KKT traces within 1e-4 relative; sam
 iteration count and stop reason.  Reference outputs come from tests/golden/solvers.npz
 (the compiled reference) or the CPU oracle on the same fp32-exact inputs.
 """
+import os
+
 import numpy as np
 import pytest
 
 from tests.conftest import rel_l2
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 TOL_ITER = 1e-4
@@ -235,3 +239,33 @@ def test_rl_kats(nd):
     tr = np.array([0.0, 1.0, 4.0, 4.0, 1.0, 0.0])
     rep = nd.deconv_rl(nd.conv_full(tr, hh), hh, tr.shape, nd.RlConfig(max_iters=5000, tol_rel_change=1e-6))
     assert rep.stop_reason == "converged" and rep.iterations_run < 5000
+
+
+def test_speculative_adjoint_is_bit_identical(tmp_path):
+    """The driver's speculative next-step adjoint must not change a single
+    bit: same estimates and traces with NDC_SPECULATE=0 and =1, on a batch that mixes
+    backtracking (initial step 8) and early stops (tol)."""
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_1711_11224_b200 import ndconv as nd, synth\n"
+        "x, y, h = synth.make('c1', batch=3, shape=(96, 80))\n"
+        "y[2] *= 0.0; y[2] += 1e-3\n"
+        "res = []\n"
+        "for step, tol in ((None, 0.0), (8.0, 0.0), (None, 1e-4)):\n"
+        "    cfg = nd.DeconvConfig(max_iters=40, tol_rel_objective=tol, initial_step=step)\n"
+        "    for r in nd.deconv_pg_batch(y, h, x.shape[1:], cfg):\n"
+        "        res += [r.estimate.ravel(), np.asarray(r.objective_trace), np.asarray(r.kkt_trace),\n"
+        "                np.array([r.iterations_run, r.extra.get('backtracks', 0)], float)]\n"
+        "np.save(sys.argv[1], np.concatenate(res))\n" % str(ROOT))
+    outs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, NDC_SPECULATE=v)
+        out = tmp_path / f"o{v}.npy"
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    assert outs[0].shape == outs[1].shape
+    assert outs[0].tobytes() == outs[1].tobytes()
