@@ -329,18 +329,16 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
 }
 
 // NR of the thread's RY row windows against every tap row of one staged plane.
-template <int KX, int SH, int RY, int NR>
+template <int KX, int SH, int RY, int NR, bool STRIDED>
 __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const float* base,
-                                                const float* trow, int KY, int kyA, int kyB,
+                                                const float* trow, int KY, int ky0, int kys,
                                                 int pitch_s) {
   constexpr int NQ = window_quads(KX, SH);
   constexpr int KXP = tap_pitch(KX);
-  // ky from 0: a uniform induction variable keeps the tap loads on the uniform datapath
-  // (LDCU -> FFMA R, R, UR); [kyA, kyB) is warp-uniform (see the caller).
-  for (int ky = 0; ky < KY; ++ky) {
-#if defined(NDC_KY_SKIP)
-    if (ky < kyA || ky >= kyB) continue;
-#endif
+  // Tap rows 0..KY-1 (STRIDED, edge tiles only: ky0, ky0 + kys, ...).  In the interior
+  // kernel the induction variable is uniform, which keeps the tap loads on the uniform
+  // datapath (LDCU -> FFMA R, R, UR).
+  for (int ky = STRIDED ? ky0 : 0; ky < KY; ky += STRIDED ? kys : 1) {
     const float* w = trow + ky * KXP;
 #if defined(NDC_J_NOUNROLL)
 #pragma unroll 1
@@ -385,7 +383,16 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
 template <int KX>
 constexpr int min_blocks_for() { return KX <= NDC_SMALL_KX ? NDC_SMALL_MIN_BLOCKS : NDC_MIN_BLOCKS; }
 
-template <int KX, int SH, int RY>
+// EDGE = false: the full tiles (tx < full_tx, ty < full_ty).  EDGE = true: the partial
+// tiles of extents that are not tile multiples (last tile column / row).  An edge tile has
+// only S < 4 column strips / R < 2 row blocks with outputs; its 8 warps are spread over
+// the S*R active (strip, block) pairs and the warps sharing a pair split the tap rows
+// (phase, nph), folded through shared memory before the epilogue -- an edge CTA then
+// finishes in proportion to its work instead of holding an SM slot for a full tile's
+// time with idle warps (config 3 forward: 47 -> 52 TFLOP/s).  Two instantiations keep the
+// interior kernel's code free of the edge logic (sharing it moved the taps off the
+// uniform datapath: -12 % on config 4).
+template <int KX, int SH, int RY, bool EDGE>
 __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     correlate_kernel(const __grid_constant__ CUtensorMap map, const CorrGeom g, const CorrArgs a,
                      const __grid_constant__ TapBlock taps) {
@@ -395,16 +402,41 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   const int b = blockIdx.z;
   if (a.active != nullptr && a.active[b] == 0) return;
   const int oz = blockIdx.y;
-  const int tile = blockIdx.x;
-  const int tx0 = (tile % g.tiles_x) * kTileX;
-  const int ty0 = (tile / g.tiles_x) * TY;
+  int txi, tyi;
+  if (!EDGE) {
+    txi = blockIdx.x % g.full_tx;
+    tyi = blockIdx.x / g.full_tx;
+  } else {
+    const int ncol = g.tiles_x - g.full_tx;  // 0 or 1 partial tile columns
+    const int e = blockIdx.x;
+    if (e < ncol * g.tiles_y) {
+      txi = g.full_tx + e / g.tiles_y;
+      tyi = e % g.tiles_y;
+    } else {
+      const int e2 = e - ncol * g.tiles_y;
+      tyi = g.full_ty + e2 / g.full_tx;
+      txi = e2 % g.full_tx;
+    }
+  }
+  const int tile = tyi * g.tiles_x + txi;
+  const int tx0 = txi * kTileX;
+  const int ty0 = tyi * TY;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   // warp index broadcast from lane 0 so the compiler treats per-warp decisions as
   // warp-uniform (keeps the tap loads on the uniform datapath under those branches)
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int wx = warp & 3;
-  const int wy = warp >> 2;
+  int wx = warp & 3, wy = warp >> 2, pw = warp, phase = 0, nph = 1, P = 8;
+  if (EDGE) {
+    const int S = min(4, (g.out_ex - tx0 + kRX - 1) / kRX);
+    const int R = min(2, (g.out_ey - ty0 + 32 * RY - 1) / (32 * RY));
+    P = S * R;
+    pw = __shfl_sync(0xffffffffu, warp % P, 0);
+    phase = __shfl_sync(0xffffffffu, warp / P, 0);
+    nph = (7 - pw) / P + 1;
+    wx = __shfl_sync(0xffffffffu, pw % S, 0);
+    wy = __shfl_sync(0xffffffffu, pw / S, 0);
+  }
 
   // Tap slices whose input plane iz = oz + kz + off_z exists (out-of-range planes are
   // skipped, which also balances edge z-slabs).
@@ -435,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // Small PSFs: prefetch the epilogue's aux_in strip (Y or x) into shared memory now,
   // so it arrives during the FFMA loop instead of stalling the epilogue.
   const float* wpre = nullptr;
-  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode)) {
+  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0) {
     float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
                  warp * (RY * 32 * kRX);
     const int ox0 = tx0 + wx * kRX;
@@ -471,19 +503,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   for (int j = 0; j < RY; ++j)
     if (ty0 + wy * (32 * RY) + 32 * j < g.out_ey) nrun = j + 1;
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
-  // Tap rows whose input row lies outside the data for every row this warp computes
-  // multiply only zero fill (forward pass near the y borders).  Data row of (output row
-  // r, tap row ky) = r + ky + off_y - in_row0.
-  int kyA = 0, kyB = g.KY;
-#if defined(NDC_KY_SKIP)
-  {
-    const int rw = ty0 + wy * (32 * RY);
-    const int dd = g.off_y - g.in_row0;
-    const int span = 32 * (nrun > 0 ? nrun : 1);
-    kyA = max(0, -dd - rw - span + 1);
-    kyB = min(g.KY, g.in_ey - dd - rw);
-  }
-#endif
   for (int i = 0; i < n; ++i) {
     const int s = i % g.stages;
     mbar_wait(&bars[s], static_cast<uint32_t>((i / g.stages) & 1));
@@ -491,9 +510,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
         reinterpret_cast<const float*>(smem_raw + s * sbytes) + row_l * g.pitch_s + wx * kRX;
     const float* trow = taps.t + (kzA + i - g.kz0) * g.KY * tap_pitch(KX);
     if (nrun == RY)
-      accumulate_rows<KX, SH, RY, RY>(acc, base, trow, g.KY, kyA, kyB, g.pitch_s);
+      accumulate_rows<KX, SH, RY, RY, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
     else if (RY > 1 && nrun == 1)
-      accumulate_rows<KX, SH, RY, 1>(acc, base, trow, g.KY, kyA, kyB, g.pitch_s);
+      accumulate_rows<KX, SH, RY, 1, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
     if (i + g.stages < n) {
       __syncthreads();  // every warp is done with stage s before it is refilled
       if (tid == 0) {
@@ -505,13 +524,45 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     }
   }
 
+  if (EDGE && P < 8) {
+    // fold the tap-row phases of each (strip, block) pair into its phase-0 warp, in
+    // phase order (deterministic), through the now idle stage buffers
+    __syncthreads();  // every warp is past its last staged plane
+    float* red = reinterpret_cast<float*>(smem_raw);
+    if (phase > 0) {
+#pragma unroll
+      for (int j = 0; j < RY; ++j)
+#pragma unroll
+        for (int q = 0; q < kRX / 4; ++q)
+          *reinterpret_cast<float4*>(red + (warp * RY + j) * (32 * kRX) + stage_pos(lane, q)) =
+              make_float4(acc[j][4 * q], acc[j][4 * q + 1], acc[j][4 * q + 2], acc[j][4 * q + 3]);
+    }
+    __syncthreads();
+    if (phase == 0) {
+      for (int k = 1; k < nph; ++k) {
+        const int w2 = pw + k * P;
+#pragma unroll
+        for (int j = 0; j < RY; ++j)
+#pragma unroll
+          for (int q = 0; q < kRX / 4; ++q) {
+            const float4 v =
+                *reinterpret_cast<const float4*>(red + (w2 * RY + j) * (32 * kRX) + stage_pos(lane, q));
+            acc[j][4 * q] += v.x;
+            acc[j][4 * q + 1] += v.y;
+            acc[j][4 * q + 2] += v.z;
+            acc[j][4 * q + 3] += v.w;
+          }
+      }
+    }
+  }
+
   // ---- epilogue (one instantiation per mode: the dispatch happens once per tile) --------
   float* wst = reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
   double p0 = 0.0, p1 = 0.0;
 #define NDC_EPI(M) \
   epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, wst, \
                                              wpre, p0, p1)
-  switch (g.final_chunk ? g.mode : -1) {
+  switch (phase != 0 ? -2 : g.final_chunk ? g.mode : -1) {  // -2: folded into a phase-0 warp
     case kEpiStore: NDC_EPI(kEpiStore); break;
     case kEpiResid: NDC_EPI(kEpiResid); break;
     case kEpiNorm: NDC_EPI(kEpiNorm); break;
@@ -520,7 +571,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     case kEpiClamp: NDC_EPI(kEpiClamp); break;
     case kEpiRLRatio: NDC_EPI(kEpiRLRatio); break;
     case kEpiRLUpdate: NDC_EPI(kEpiRLUpdate); break;
-    default: NDC_EPI(-1); break;
+    case -1: NDC_EPI(-1); break;
+    default: break;
   }
 #undef NDC_EPI
 
@@ -547,13 +599,23 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
                       ((KX <= NDC_STAGED_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY>,
+    cudaError_t e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(g.tiles_x * g.tiles_y, nz_out, batch);
-  correlate_kernel<KX, SH, RY><<<grid, kThreads, smem, s>>>(map, g, a, taps);
+  // full tiles, then the partial last tile column / row
+  const int n_full = g.full_tx * g.full_ty;
+  const int n_edge = g.tiles_x * g.tiles_y - n_full;
+  if (n_full > 0) {
+    correlate_kernel<KX, SH, RY, false><<<dim3(n_full, nz_out, batch), kThreads, smem, s>>>(map, g, a, taps);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  }
+  if (n_edge > 0)
+    correlate_kernel<KX, SH, RY, true><<<dim3(n_edge, nz_out, batch), kThreads, smem, s>>>(map, g, a, taps);
   return cudaGetLastError();
 }
 

@@ -62,6 +62,7 @@ struct CorrGeom {
   int KY;              // tap rows per z-slice
   int kz0, kz1;        // z-slices of the taps carried by this launch
   int tiles_x, tiles_y;
+  int full_tx, full_ty;  // tile columns / rows wholly inside the output
   int rows, pitch_s;   // shared tile: rows x pitch_s floats per stage
   int stages;
   int aux_prefetch;    // cp.async the epilogue's aux_in strip at kernel start (small PSFs)

@@ -531,6 +531,10 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   g.KY = KY_;
   g.tiles_x = static_cast<int>(cdiv(vout.ex, kTileX));
   g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY * ry_));
+  // partial edge tiles run as a second launch with the edge kernel (ndc_correlate.cuh);
+  // HBM-bound small PSFs keep one launch (the edge kernel's gain is compute-side)
+  g.full_tx = KX_ <= kSmallMaxKX ? g.tiles_x : vout.ex / kTileX;
+  g.full_ty = KX_ <= kSmallMaxKX ? g.tiles_y : vout.ey / (kTileY * ry_);
   g.rows = kTileY * ry_ + KY_ - 1;
   g.pitch_s = shared_pitch_for(KX_, sh);
   g.out_pitch = vout.pitch;
