@@ -170,7 +170,7 @@ class Clocks:
 WORK = {
     "c2": dict(e2e_iters=100, steps=30, step=None, desc="16x2048x2048 2D batch, PSF 31x31 sigma 4, Poisson 1000"),
     "c3": dict(e2e_iters=50, steps=20, step=None, desc="3D 256x256x128, PSF 15x15x31 sigma_xy 1.5 sigma_z 4"),
-    "c4": dict(e2e_iters=4, steps=5, step=1.0, desc="3D 1024x1024x512, PSF 9x9x21, Poisson 500"),
+    "c4": dict(e2e_iters=30, steps=5, step=1.0, desc="3D 1024x1024x512, PSF 9x9x21, Poisson 500"),
     "c5": dict(e2e_iters=2, steps=2, step=1.0, desc="3D 2048x2048x256, 33x33x65 3-Gaussian PSF, Poisson 200"),
     # HBM-bound small-PSF case (not a BASELINE config; north_star's ">= 70 % HBM" target)
     "c2s": dict(e2e_iters=100, steps=500, step=None,
