@@ -18,8 +18,9 @@
  * without a usable B200 the compute entry points return NDC_ERR_NO_DEVICE.
  *
  * Supported operands on the device path: 1 <= ndim <= 3 (plus the batch index of
- * the *_batch entry points), kernel x-extent <= 33, kernel y-extent <= 193; other
- * odd kernels return NDC_ERR_UNSUPPORTED.
+ * the *_batch entry points) and odd kernels of any size (PSFs beyond one launch's tap
+ * block -- 33 columns, the rows of one TMA box, 7680 taps -- run as several accumulated
+ * launches).
  */
 #ifndef NDCONV_B200_H
 #define NDCONV_B200_H

@@ -95,15 +95,14 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   pz_ = (KZ_ - 1) / 2;
   py_ = (KY_ - 1) / 2;
   px_ = (KX_ - 1) / 2;
-  if (KX_ > kMaxKX)
-    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: kernel x-extent " + std::to_string(KX_) + " > " +
-                                  std::to_string(kMaxKX));
-  if (kTileY + KY_ - 1 > kMaxRows)
-    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: kernel y-extent " + std::to_string(KY_) + " too large");
-  if (KY_ * tap_pitch(KX_) > kTapCap)
-    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: one kernel z-slice exceeds the per-launch tap block");
   if (static_cast<long long>(my_) + 2 * py_ > (1 << 30) || static_cast<long long>(mx_) + 2 * px_ > (1 << 30))
     fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: extent too large");
+  // Kernels of any odd size: a launch carries a tap block of at most kMaxKX columns x
+  // kcy_ rows x (as many z-slices as fit kTapCap); larger PSFs run as several launches
+  // accumulated through a scratch volume (see correlate()).  Column chunks start at
+  // multiples of 32 (keeps the TMA tile origin 16-byte aligned) and are padded with zero
+  // taps to an instantiated odd width.
+  kcx_ = KX_ <= kMaxKX ? KX_ : kMaxKX;
   // Two output rows per thread (tile height 128) halves the per-row tap loads and loop
   // overhead; used for single-plane (2-D / batched) problems whose 128+KY-1 staged rows
   // fit one TMA box.  3-D volumes keep 64-row tiles so two plane stages fit beside a
@@ -113,7 +112,7 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   // 128-row stages would drop residency to one CTA).
   stages_ = (KZ_ > 1) ? 2 : 1;
   {
-    const long long pitch2 = std::max(shared_pitch_for(KX_, 0), shared_pitch_for(KX_, 2));
+    const long long pitch2 = std::max(shared_pitch_for(kcx_, 0), shared_pitch_for(kcx_, 2));
     const long long stage2 = static_cast<long long>(2 * kTileY + KY_ - 1) * pitch2 * 4;
     const bool fits = 2 * kTileY + KY_ - 1 <= kMaxRows;
     ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= 90 * 1024)) ? 2 : 1;
@@ -121,6 +120,7 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     if (KX_ <= kSmallMaxKX) ry_ = 1;
   }
   if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
+  kcy_ = std::min(KY_, kMaxRows - kTileY * ry_ + 1);  // staged rows 64*ry + kcy - 1 <= TMA box limit
 
   if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
 
@@ -447,8 +447,9 @@ void Plan::alloc_all() {
   yobs_ = dev_alloc_f(ny);
   r_ = dev_alloc_f(ny);
   rt_ = dev_alloc_f(ny);
-  const int slices_per = kTapCap / (KY_ * tap_pitch(KX_));
-  if (KZ_ > slices_per) scratch_ = dev_alloc_f(std::max(nx, ny));
+  // partial sums of multi-launch (chunked) PSFs, see correlate()
+  const bool chunked = KX_ > kMaxKX || KY_ > kcy_ || KZ_ > kTapCap / (KY_ * tap_pitch(KX_));
+  if (chunked) scratch_ = dev_alloc_f(std::max(nx, ny));
   partials_cap_ = static_cast<long long>(B_) *
                   std::max({partials_per_image(kFwd), partials_per_image(kAdj),
                             static_cast<long long>(kElemBlocks)});
@@ -480,8 +481,8 @@ void Plan::alloc_all() {
 
 void Plan::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
-const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh) {
-  auto key = std::make_pair(base, static_cast<int>(d));
+const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh, int kx, int ky) {
+  auto key = std::make_pair(base, static_cast<int>(d) + 2 * (kx + 64 * ky));
   auto it = maps_.find(key);
   if (it != maps_.end()) return it->second;
   const Vol& v = (d == kFwd) ? X_ : Y_;
@@ -489,7 +490,7 @@ const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh) {
   // x-shaped inputs are described including their zero margin (ndc_plan.h Vol)
   const CUresult rc = encode_tensor_map(&m, base, v.c0 + v.ex, v.r0 + v.ey,
                                         static_cast<long long>(v.ez) * B_, v.pitch, v.plane,
-                                        shared_pitch_for(KX_, sh), kTileY * ry_ + KY_ - 1);
+                                        shared_pitch_for(kx, sh), kTileY * ry_ + ky - 1);
   if (rc != CUDA_SUCCESS)
     fail(NDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(rc)) + ")");
   return maps_.emplace(key, m).first->second;
@@ -528,31 +529,48 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   // TMA tile starts must be non-negative (x-shaped inputs carry a zero margin)
   if (g.off_x < 0 || g.off_y < 0 || (g.off_x & 3))
     fail(NDC_ERR_CUDA, "internal: negative or unaligned TMA tile origin");
-  g.KY = KY_;
   g.tiles_x = static_cast<int>(cdiv(vout.ex, kTileX));
   g.tiles_y = static_cast<int>(cdiv(vout.ey, kTileY * ry_));
   // partial edge tiles run as a second launch with the edge kernel (ndc_correlate.cuh);
   // HBM-bound small PSFs keep one launch (the edge kernel's gain is compute-side)
   g.full_tx = KX_ <= kSmallMaxKX ? g.tiles_x : vout.ex / kTileX;
   g.full_ty = KX_ <= kSmallMaxKX ? g.tiles_y : vout.ey / (kTileY * ry_);
-  g.rows = kTileY * ry_ + KY_ - 1;
-  g.pitch_s = shared_pitch_for(KX_, sh);
   g.out_pitch = vout.pitch;
   g.out_plane = vout.plane;
   g.out_image = vout.image;
   g.mode = mode;
-  const int per_slice = KY_ * tap_pitch(KX_);
-  const int slices_per = kTapCap / per_slice;
-  const int nchunks = static_cast<int>(cdiv(KZ_, slices_per));
-  const CUtensorMap& map = map_for(in, d, sh);
+  const int off_x0 = g.off_x, off_y0 = g.off_y;
+  const int kxp_full = tap_pitch(KX_);
+  // Tap chunks: columns [kx0, kx0 + cw) (instantiation width w >= cw, zero padded), rows
+  // [ky0, ky0 + cy), z-slices [kz0, kz1).  One chunk for every PSF up to 33 columns,
+  // kcy_ rows and kTapCap taps (all BASELINE configs but config 5, which splits in z).
+  struct Chunk {
+    int kx0, cw, w, ky0, cy, kz0, kz1;
+  };
+  std::vector<Chunk> chunks;
+  for (int kx0 = 0; kx0 < KX_; kx0 += (KX_ <= kMaxKX ? KX_ : kMaxKX - 1)) {
+    const int cw = KX_ <= kMaxKX ? KX_ : std::min(kMaxKX - 1, KX_ - kx0);
+    const int w = (cw % 2) ? cw : cw + 1;
+    for (int ky0 = 0; ky0 < KY_; ky0 += kcy_) {
+      const int cy = std::min(kcy_, KY_ - ky0);
+      const int slices = std::max(1, kTapCap / (cy * tap_pitch(w)));
+      for (int kz0 = 0; kz0 < KZ_; kz0 += slices) chunks.push_back({kx0, cw, w, ky0, cy, kz0, std::min(KZ_, kz0 + slices)});
+    }
+  }
   static thread_local TapBlock tb;
-  for (int c = 0; c < nchunks; ++c) {
-    g.kz0 = c * slices_per;
-    g.kz1 = std::min(KZ_, g.kz0 + slices_per);
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const Chunk& ch = chunks[c];
+    g.KY = ch.cy;
+    g.rows = kTileY * ry_ + ch.cy - 1;
+    g.pitch_s = shared_pitch_for(ch.w, sh);
+    g.off_x = off_x0 + ch.kx0;  // multiples of 32: the TMA origin stays 16-byte aligned
+    g.off_y = off_y0 + ch.ky0;
+    g.kz0 = ch.kz0;
+    g.kz1 = ch.kz1;
     g.stages = std::min(stages_, g.kz1 - g.kz0);
     g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
     g.accum = c > 0;
-    g.final_chunk = (c == nchunks - 1);
+    g.final_chunk = (c + 1 == chunks.size());
     // x-shaped operands are addressed from their interior origin
     const long long xo = fwd ? 0 : X_.origin;
     auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
@@ -565,8 +583,20 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     a.step = step;
     a.active = active;
     a.partials = (g.final_chunk && partials) ? partials_ : nullptr;
-    std::memcpy(tb.t, taps.data() + static_cast<size_t>(g.kz0) * per_slice,
-                static_cast<size_t>(g.kz1 - g.kz0) * per_slice * sizeof(float));
+    // gather the chunk's taps [kz][ky][kx] with row pitch tap_pitch(w), zero padded
+    const int wp = tap_pitch(ch.w);
+    if (ch.kx0 == 0 && ch.w == KX_ && ch.cy == KY_) {
+      std::memcpy(tb.t, taps.data() + static_cast<size_t>(ch.kz0) * KY_ * kxp_full,
+                  static_cast<size_t>(ch.kz1 - ch.kz0) * KY_ * kxp_full * sizeof(float));
+    } else {
+      for (int kz = ch.kz0; kz < ch.kz1; ++kz)
+        for (int ky = 0; ky < ch.cy; ++ky) {
+          float* dst = tb.t + (static_cast<size_t>(kz - ch.kz0) * ch.cy + ky) * wp;
+          const float* src = taps.data() + (static_cast<size_t>(kz) * KY_ + ch.ky0 + ky) * kxp_full + ch.kx0;
+          for (int kx = 0; kx < wp; ++kx) dst[kx] = kx < ch.cw ? src[kx] : 0.0f;
+        }
+    }
+    const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
     size_t ev = 0;
     if (timing_) {
       if (ev_used_ == ev_pool_.size()) {
@@ -578,7 +608,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
       ev = ev_used_++;
       check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
     }
-    check_cuda(launch_correlate(KX_, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
+    check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
                "correlate launch");
     if (timing_) {
       check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");

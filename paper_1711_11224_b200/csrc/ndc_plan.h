@@ -132,7 +132,7 @@ class Plan {
   void d2h_staged(void* host, const void* dev, size_t bytes);
   void* hpin_[2] = {nullptr, nullptr};      // pinned staging ring (16 MB slots)
   cudaEvent_t pin_ev_[2] = {nullptr, nullptr};
-  const CUtensorMap& map_for(const float* base, Dir d, int sh);
+  const CUtensorMap& map_for(const float* base, Dir d, int sh, int kx, int ky);
   // Correlation pass over resident buffers; mode / aux per EpiMode.
   void correlate(Dir d, const float* in, float* out, int mode, float* aux_out, const float* aux_in,
                  const float* scale, const double* step, const int* active, bool partials);
@@ -164,6 +164,7 @@ class Plan {
   size_t xext_[3] = {1, 1, 1}, kext_[3] = {1, 1, 1};
   int mz_ = 1, my_ = 1, mx_ = 1;
   int KZ_ = 1, KY_ = 1, KX_ = 1, pz_ = 0, py_ = 0, px_ = 0;
+  int kcx_ = 1, kcy_ = 1;  // tap-chunk extents of one launch (x <= kMaxKX, rows <= TMA box)
   int ry_ = 1;      // output rows per thread in the correlation kernel (tile height 64*ry)
   int stages_ = 1;  // TMA plane stages in flight per CTA
   std::vector<float> taps_fwd_, taps_adj_;

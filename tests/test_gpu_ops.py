@@ -134,7 +134,27 @@ def test_error_classes(nd):
     with pytest.raises(nd.Error):
         nd.deconv_pg(np.zeros(6), [0.1, 0.8, 0.1], (4,), nd.DeconvConfig(max_iters=0))
     with pytest.raises(nd.UnsupportedError):
-        nd.conv_full(np.ones((4, 4)), np.ones((3, 35)))
+        nd.conv_full(np.ones((2, 2, 2, 2)), np.ones((1, 1, 1, 1)))  # the device path is 1- to 3-d
+
+
+@pytest.mark.parametrize("xs,hs", [((37, 50), (3, 35)), ((60, 90), (37, 71)), ((50, 40), (201, 3)),
+                                   ((9, 30, 70), (3, 5, 67)), ((140,), (99,)), ((30, 260), (5, 129))])
+def test_large_psfs_chunked(nd, oracle_c, xs, hs):
+    """PSFs beyond one launch's tap block (more than 33 columns, more rows than one TMA box
+    holds) run as several chunk launches accumulated on the device; forward, adjoint and
+    a short PG run against the oracle."""
+    rng = np.random.default_rng(sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    assert rel_l2(nd.conv_full(x, h), oracle_c.conv_full(x, h)) <= 1e-5
+    y = oracle_c.conv_full(x, h) + rng.uniform(0, 1e-3, nd.conv_output_shape(xs, h))
+    assert rel_l2(nd.adjoint_apply(y, h, xs), oracle_c.adjoint_apply(y, h, xs)) <= 1e-5
+    cfg = nd.DeconvConfig(max_iters=5, tol_rel_objective=0.0, initial_step=1.0)
+    got = nd.deconv_pg(y, h, xs, cfg)
+    want = oracle_c.deconv_pg(y, h, xs, max_iters=5, tol_rel_objective=0.0, initial_step=1.0)
+    assert got.iterations_run == want.iterations_run
+    assert rel_l2(got.estimate, want.estimate) <= 1e-4
 
 
 def test_config_shapes_sampled(nd, oracle_c):
