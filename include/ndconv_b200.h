@@ -112,6 +112,13 @@ ndc_status ndc_conv_full_f64(int ndim, const size_t* x_ext, const double* x, con
                              const double* h, double* y);
 
 /* convolution.hpp:166-174 adjoint_apply: x_out (x_ext) = A^T y (y_ext == x_ext + 2p). */
+/* Batched float32 operators (a leading batch index of independent images): y[b] = A x[b]
+ * and x[b] = A^T y[b] -- for callers that keep float data (no f64 round trip). */
+ndc_status ndc_conv_full_batch_f32(size_t batch, int ndim, const size_t* x_ext, const float* x,
+                                   const size_t* k_ext, const double* h, float* y);
+ndc_status ndc_adjoint_apply_batch_f32(size_t batch, int ndim, const size_t* y_ext, const float* y,
+                                       const size_t* k_ext, const double* h, const size_t* x_ext,
+                                       float* x_out);
 ndc_status ndc_adjoint_apply_f64(int ndim, const size_t* y_ext, const double* y,
                                  const size_t* k_ext, const double* h, const size_t* x_ext,
                                  double* x_out);

@@ -98,6 +98,9 @@ _SIGS = [
     ("ndc_ndtensor_write_f64", C.c_int, [C.c_char_p, C.c_int, size_t_p, dbl_p]),
     ("ndc_pgm_info", C.c_int, [C.c_char_p, size_t_p, size_t_p]),
     ("ndc_pgm_read_f64", C.c_int, [C.c_char_p, dbl_p, C.c_size_t]),
+    ("ndc_conv_full_batch_f32", C.c_int, [C.c_size_t, C.c_int, size_t_p, flt_p, size_t_p, dbl_p, flt_p]),
+    ("ndc_adjoint_apply_batch_f32", C.c_int, [C.c_size_t, C.c_int, size_t_p, flt_p, size_t_p, dbl_p, size_t_p,
+                                              flt_p]),
     ("ndc_pgm_write_f64", C.c_int, [C.c_char_p, C.c_size_t, C.c_size_t, dbl_p, C.c_int]),
     ("ndc_plan_get_observation_f64", C.c_int, [C.c_void_p, dbl_p]),
     ("ndc_plan_add_gaussian_noise", C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_uint64]),

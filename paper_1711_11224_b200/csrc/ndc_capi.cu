@@ -171,6 +171,37 @@ ndc_status ndc_conv_full_f64(int ndim, const size_t* x_ext, const double* x, con
   });
 }
 
+ndc_status ndc_conv_full_batch_f32(size_t batch, int ndim, const size_t* x_ext, const float* x,
+                                   const size_t* k_ext, const double* h, float* y) {
+  return guard([&] {
+    check_ndim(ndim);
+    need(x, "x");
+    need(h, "h");
+    need(y, "y");
+    auto p = one_shot(batch, ndim, x_ext, k_ext, h);
+    p->set_x_f32(x);
+    p->op_conv_full();
+    p->get_y_buffer_f32(y);
+  });
+}
+ndc_status ndc_adjoint_apply_batch_f32(size_t batch, int ndim, const size_t* y_ext, const float* y,
+                                       const size_t* k_ext, const double* h, const size_t* x_ext,
+                                       float* x_out) {
+  return guard([&] {
+    check_ndim(ndim);
+    need(y, "y");
+    need(h, "h");
+    need(x_out, "x_out");
+    for (int i = 0; i < ndim; ++i)
+      if (y_ext[i] != x_ext[i] + k_ext[i] - 1)
+        ndc::fail(NDC_ERR_SHAPE, "adjoint_apply: observation shape is not x_shape + 2p");
+    check_forward(ndim, y_ext, k_ext, x_ext, "adjoint_apply");
+    auto p = one_shot(batch, ndim, x_ext, k_ext, h);
+    p->set_observation_f32(y);
+    p->op_adjoint_of_y();
+    p->get_x_buffer_f32(x_out);
+  });
+}
 ndc_status ndc_adjoint_apply_f64(int ndim, const size_t* y_ext, const double* y, const size_t* k_ext,
                                  const double* h, const size_t* x_ext, double* x_out) {
   return guard([&] {

@@ -849,6 +849,12 @@ void Plan::set_x_f64(const double* x) {
   pack_dense_f64(x, x_, X_, xa_ - xlo_, xa_n_);
   halo_x(x_);
 }
+void Plan::set_x_f32(const float* x) {
+  pack_dense_f32(x, x_, X_, xa_ - xlo_, xa_n_);
+  halo_x(x_);
+}
+void Plan::get_y_buffer_f32(float* y) { unpack_dense_f32(r_, y, Y_, ya_ - rlo_, yb_ - ya_); }
+void Plan::get_x_buffer_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
 void Plan::get_estimate_f64(double* x) { unpack_dense_f64(x_, x, X_, xa_ - xlo_, xa_n_); }
 void Plan::get_estimate_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
 void Plan::get_observation_f64(double* y) { unpack_dense_f64(yobs_, y, Y_, ya_ - rlo_, yb_ - ya_); }

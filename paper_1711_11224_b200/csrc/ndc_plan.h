@@ -76,10 +76,13 @@ class Plan {
   void set_observation_f64(const double* y);
   void set_observation_f32(const float* y);
   void set_x_f64(const double* x);               // into the x buffer (for conv_full etc.)
+  void set_x_f32(const float* x);
   void get_estimate_f64(double* x);
   void get_estimate_f32(float* x);
   void get_observation_f64(double* y);           // the resident (f32) observation
   void get_y_buffer_f64(double* y);              // the y-shaped result buffer (A x)
+  void get_y_buffer_f32(float* y);
+  void get_x_buffer_f32(float* x);
   void get_x_buffer_f64(double* x, int which);   // 0 = x, 1 = g
   void load_observation_ndtensor(const std::string& path);  // streamed, owned planes
   void save_estimate_ndtensor(const std::string& path);

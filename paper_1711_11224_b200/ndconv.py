@@ -168,6 +168,31 @@ def conv_full(x, h) -> np.ndarray:
     return y
 
 
+def conv_full_batch(x, h) -> np.ndarray:
+    """y[b] = conv_full(x[b], h) for a float32 batch x[b, ...] (ndc_conv_full_batch_f32)."""
+    h = _kernel(h)
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim != h.ndim + 1:
+        raise ShapeError("conv_full: dimension count mismatch")
+    ys = conv_output_shape(x.shape[1:], h)
+    y = np.empty((x.shape[0],) + ys, np.float32)
+    _check(N.lib().ndc_conv_full_batch_f32(x.shape[0], h.ndim, _ext(x.shape[1:]), _pf(x), _ext(h.shape), _p(h),
+                                           _pf(y)))
+    return y
+
+
+def adjoint_apply_batch(y, h, x_shape) -> np.ndarray:
+    """x[b] = adjoint_apply(y[b], h, x_shape) for a float32 batch (ndc_adjoint_apply_batch_f32)."""
+    h = _kernel(h)
+    y = np.ascontiguousarray(y, np.float32)
+    if y.ndim != h.ndim + 1 or len(x_shape) != h.ndim:
+        raise ShapeError("adjoint_apply: dimension count mismatch")
+    x = np.empty((y.shape[0],) + tuple(int(v) for v in x_shape), np.float32)
+    _check(N.lib().ndc_adjoint_apply_batch_f32(y.shape[0], h.ndim, _ext(y.shape[1:]), _pf(y), _ext(h.shape), _p(h),
+                                               _ext(x_shape), _pf(x)))
+    return x
+
+
 def flip(h) -> np.ndarray:
     """kernel.hpp:41-45: reversal along every axis (the reversed flat buffer)."""
     h = _kernel(h)

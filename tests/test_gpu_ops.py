@@ -174,3 +174,20 @@ def test_config_shapes_sampled(nd, oracle_c):
         idx = g.integers(0, a.size, 3000)
         ref = oracle_c.adjoint_sample(r, h, shape, idx)
         assert rel_l2(a.ravel()[idx], ref) <= TOL_CONV, name
+
+
+def test_batched_float32_operators(nd, oracle_c):
+    """ndc_conv_full_batch_f32 / ndc_adjoint_apply_batch_f32: every image of the batch as
+    the f64 single-image operator (float32 in and out)."""
+    rng = np.random.default_rng(77)
+    for xs, hs in (((3, 70, 90), (7, 9)), ((2, 12, 30, 40), (5, 3, 7)), ((4, 500), (41,))):
+        x = rng.uniform(0, 1, xs).astype(np.float32)
+        h = rng.uniform(0, 1, hs)
+        y = nd.conv_full_batch(x, h)
+        assert y.dtype == np.float32 and y.shape == (xs[0],) + nd.conv_output_shape(xs[1:], h)
+        for b in range(xs[0]):
+            assert rel_l2(y[b], oracle_c.conv_full(x[b].astype(np.float64), h)) <= 1e-5
+        r = rng.uniform(-1, 1, y.shape).astype(np.float32)
+        g = nd.adjoint_apply_batch(r, h, xs[1:])
+        for b in range(xs[0]):
+            assert rel_l2(g[b], oracle_c.adjoint_apply(r[b].astype(np.float64), h, xs[1:])) <= 1e-5
