@@ -401,7 +401,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
 
   const int b = blockIdx.z;
   if (a.active != nullptr && a.active[b] == 0) return;
-  const int oz = blockIdx.y;
+  // computed output plane: launches may cover a subset of the pass's planes (z-slab
+  // ranks run the planes that need no halo first, ndc_plan.cu correlate())
+  const int oz = static_cast<int>(blockIdx.y) + g.z_base + (static_cast<int>(blockIdx.y) >= g.z_gap_at ? g.z_gap : 0);
   int txi, tyi;
   if (!EDGE) {
     txi = blockIdx.x % g.full_tx;
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     p1 = warp_sum(p1);
     if (lane == 0) {
       const long long idx =
-          ((static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile) *
+          ((static_cast<long long>(b) * g.part_nz + oz) * (g.tiles_x * g.tiles_y) + tile) *
               (kThreads / 32) + warp;
       a.partials[idx] = make_double2(p0, p1);
     }

@@ -69,6 +69,9 @@ struct CorrGeom {
   int accum;           // add the partial sum held in `accum_in`
   int mode;            // EpiMode (ignored unless final)
   int final_chunk;     // last tap chunk: apply the epilogue
+  // planes of this launch: computed index oz = blockIdx.y + z_base (+ z_gap once
+  // blockIdx.y >= z_gap_at); part_nz = computed planes of the whole pass (partials index)
+  int z_base, z_gap_at, z_gap, part_nz;
   long long out_pitch, out_plane, out_image;  // in floats
 };
 

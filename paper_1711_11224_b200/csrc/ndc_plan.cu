@@ -178,12 +178,18 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   if (prop.major != 10)
     fail(NDC_ERR_NO_DEVICE, std::string("ndconv_b200: built for sm_100a, device is ") + prop.name);
   check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (world_ > 1) {
+    check_cuda(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaEventCreateWithFlags(&pass_ev_, cudaEventDisableTiming), "cudaEventCreate");
+    if (const char* e = std::getenv("NDC_HALO_OVERLAP")) halo_overlap_ = std::atoi(e) != 0;
+  }
   alloc_all();
 }
 
 Plan::~Plan() {
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
+  if (comm_stream_) cudaStreamSynchronize(comm_stream_);  // halo sends read plan buffers
   for (auto& e : ev_pool_) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -197,6 +203,11 @@ Plan::~Plan() {
                   staging_})
     if (p) cudaFreeAsync(p, stream_);
   if (stream_) cudaStreamSynchronize(stream_);
+  if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+  for (auto& e : halo_ev_)
+    if (e.second) cudaEventDestroy(e.second);
+  if (pass_ev_) cudaEventDestroy(pass_ev_);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
   if (hsc_) small_pinned_put(small_bytes_, hsc_);
   if (up_ev_) cudaEventDestroy(up_ev_);
   if (d2h_ev_) cudaEventDestroy(d2h_ev_);
@@ -479,7 +490,10 @@ void Plan::alloc_all() {
   sync();
 }
 
-void Plan::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+void Plan::sync() {
+  drain_halos();  // the plan stream then covers the comm stream too
+  check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
 
 const CUtensorMap& Plan::map_for(const float* base, Dir d, int sh, int kx, int ky) {
   auto key = std::make_pair(base, static_cast<int>(d) + 2 * (kx + 64 * ky));
@@ -558,64 +572,91 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     }
   }
   static thread_local TapBlock tb;
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    const Chunk& ch = chunks[c];
-    g.KY = ch.cy;
-    g.rows = kTileY * ry_ + ch.cy - 1;
-    g.pitch_s = shared_pitch_for(ch.w, sh);
-    g.off_x = off_x0 + ch.kx0;  // multiples of 32: the TMA origin stays 16-byte aligned
-    g.off_y = off_y0 + ch.ky0;
-    g.kz0 = ch.kz0;
-    g.kz1 = ch.kz1;
-    g.stages = std::min(stages_, g.kz1 - g.kz0);
-    g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
-    g.accum = c > 0;
-    g.final_chunk = (c + 1 == chunks.size());
-    // x-shaped operands are addressed from their interior origin
-    const long long xo = fwd ? 0 : X_.origin;
-    auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
-    CorrArgs a{};
-    a.out = at(g.final_chunk ? out : scratch_);
-    a.accum_in = at(scratch_);
-    a.aux_out = at(aux_out);
-    a.aux_in = fwd ? aux_in : at(aux_in);
-    a.scale = scale;
-    a.step = step;
-    a.active = active;
-    a.partials = (g.final_chunk && partials) ? partials_ : nullptr;
-    // gather the chunk's taps [kz][ky][kx] with row pitch tap_pitch(w), zero padded
-    const int wp = tap_pitch(ch.w);
-    if (ch.kx0 == 0 && ch.w == KX_ && ch.cy == KY_) {
-      std::memcpy(tb.t, taps.data() + static_cast<size_t>(ch.kz0) * KY_ * kxp_full,
-                  static_cast<size_t>(ch.kz1 - ch.kz0) * KY_ * kxp_full * sizeof(float));
-    } else {
-      for (int kz = ch.kz0; kz < ch.kz1; ++kz)
-        for (int ky = 0; ky < ch.cy; ++ky) {
-          float* dst = tb.t + (static_cast<size_t>(kz - ch.kz0) * ch.cy + ky) * wp;
-          const float* src = taps.data() + (static_cast<size_t>(kz) * KY_ + ch.ky0 + ky) * kxp_full + ch.kx0;
-          for (int kx = 0; kx < wp; ++kx) dst[kx] = kx < ch.cw ? src[kx] : 0.0f;
-        }
-    }
-    const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
-    size_t ev = 0;
-    if (timing_) {
-      if (ev_used_ == ev_pool_.size()) {
-        cudaEvent_t e0, e1;
-        check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
-        check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
-        ev_pool_.emplace_back(e0, e1);
+  // One launch per tap chunk over the computed planes [z_base, z_base + nz), skipping
+  // `gap` planes once `gap_at` planes are done.
+  auto run_chunks = [&](int z_base, int nz, int gap_at, int gap) {
+    for (size_t c = 0; c < chunks.size(); ++c) {
+      const Chunk& ch = chunks[c];
+      g.KY = ch.cy;
+      g.rows = kTileY * ry_ + ch.cy - 1;
+      g.pitch_s = shared_pitch_for(ch.w, sh);
+      g.off_x = off_x0 + ch.kx0;  // multiples of 32: the TMA origin stays 16-byte aligned
+      g.off_y = off_y0 + ch.ky0;
+      g.kz0 = ch.kz0;
+      g.kz1 = ch.kz1;
+      g.stages = std::min(stages_, g.kz1 - g.kz0);
+      g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
+      g.accum = c > 0;
+      g.final_chunk = (c + 1 == chunks.size());
+      g.z_base = z_base;
+      g.z_gap_at = gap_at;
+      g.z_gap = gap;
+      g.part_nz = nz_out;
+      // x-shaped operands are addressed from their interior origin
+      const long long xo = fwd ? 0 : X_.origin;
+      auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
+      CorrArgs a{};
+      a.out = at(g.final_chunk ? out : scratch_);
+      a.accum_in = at(scratch_);
+      a.aux_out = at(aux_out);
+      a.aux_in = fwd ? aux_in : at(aux_in);
+      a.scale = scale;
+      a.step = step;
+      a.active = active;
+      a.partials = (g.final_chunk && partials) ? partials_ : nullptr;
+      // gather the chunk's taps [kz][ky][kx] with row pitch tap_pitch(w), zero padded
+      const int wp = tap_pitch(ch.w);
+      if (ch.kx0 == 0 && ch.w == KX_ && ch.cy == KY_) {
+        std::memcpy(tb.t, taps.data() + static_cast<size_t>(ch.kz0) * KY_ * kxp_full,
+                    static_cast<size_t>(ch.kz1 - ch.kz0) * KY_ * kxp_full * sizeof(float));
+      } else {
+        for (int kz = ch.kz0; kz < ch.kz1; ++kz)
+          for (int ky = 0; ky < ch.cy; ++ky) {
+            float* dst = tb.t + (static_cast<size_t>(kz - ch.kz0) * ch.cy + ky) * wp;
+            const float* src = taps.data() + (static_cast<size_t>(kz) * KY_ + ch.ky0 + ky) * kxp_full + ch.kx0;
+            for (int kx = 0; kx < wp; ++kx) dst[kx] = kx < ch.cw ? src[kx] : 0.0f;
+          }
       }
-      ev = ev_used_++;
-      check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
+      const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
+      size_t ev = 0;
+      if (timing_) {
+        if (ev_used_ == ev_pool_.size()) {
+          cudaEvent_t e0, e1;
+          check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
+          check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+          ev_pool_.emplace_back(e0, e1);
+        }
+        ev = ev_used_++;
+        check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
+      }
+      check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz, stream_),
+                 "correlate launch");
+      if (timing_) {
+        check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
+        ev_pending_.emplace_back(fwd ? 0 : 1, ev);
+      }
+      st_[fwd ? 0 : 1].launches++;
+      st_[2].launches++;
     }
-    check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz_out, stream_),
-               "correlate launch");
-    if (timing_) {
-      check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
-      ev_pending_.emplace_back(fwd ? 0 : 1, ev);
-    }
-    st_[fwd ? 0 : 1].launches++;
-    st_[2].launches++;
+  };
+  // Outputs still being sent to a neighbour, or halo planes still arriving, must not be
+  // overwritten: wait for their exchange first (no-op unless an exchange is pending).
+  wait_halo(out);
+  wait_halo(aux_out);
+  // z-slab ranks: the first `lo` / last `hi` computed planes are exactly the planes that
+  // read the input's halo and the planes the neighbours need next, so the
+  // other planes run first, before waiting for the input's halo exchange (which overlaps
+  // them), then the boundary planes.
+  const int lo = (world_ > 1 && rank_ > 0) ? pz_ : 0;
+  const int hi = (world_ > 1 && rank_ + 1 < world_) ? pz_ : 0;
+  const int n_int = nz_out - lo - hi;
+  if (halo_overlap_ && (lo + hi) > 0 && n_int > 0) {
+    run_chunks(lo, n_int, nz_out, 0);
+    wait_halo(in);
+    run_chunks(0, lo + hi, lo, n_int);
+  } else {
+    wait_halo(in);
+    run_chunks(0, nz_out, nz_out, 0);
   }
 }
 
@@ -665,13 +706,21 @@ void Plan::finalize(long long per_image, int op, double* out0, double* out1, flo
 
 // Halo planes: the forward pass needs p_z x-planes from each neighbour,
 // the adjoint p_z y-planes; slabs are at least p_z thick so one neighbour suffices.
+//
+// halo_x / halo_y enqueue the exchange of `buf`'s boundary planes on the comm stream once
+// everything enqueued so far on the plan stream is done, and record a per-buffer event.
+// The plan stream does not wait for it: correlate() waits before the launch that reads
+// the halo (after the planes that do not need it), and before any launch that writes
+// `buf`; every other user of a sharded buffer drains the pending exchanges first
+// (drain_halos).  With NDC_HALO_OVERLAP=0 the plan stream waits right away (the exchange
+// is serialised with the passes, as a plain send/recv would be).
 void Plan::halo_x(float* buf) {
   if (world_ == 1 || pz_ == 0) return;
   const size_t n = static_cast<size_t>(pz_) * X_.plane;
   auto at = [&](int global_plane) { return buf + static_cast<long long>(global_plane - xlo_) * X_.plane; };
   const bool lo = rank_ > 0, hi = rank_ + 1 < world_;
-  comm_->exchange(lo ? at(xa_) : nullptr, lo ? at(xa_ - pz_) : nullptr, hi ? at(xb_ - pz_) : nullptr,
-                  hi ? at(xb_) : nullptr, n, stream_);
+  halo_enqueue(buf, lo ? at(xa_) : nullptr, lo ? at(xa_ - pz_) : nullptr, hi ? at(xb_ - pz_) : nullptr,
+               hi ? at(xb_) : nullptr, n);
 }
 
 void Plan::halo_y(float* buf) {
@@ -679,8 +728,33 @@ void Plan::halo_y(float* buf) {
   const size_t n = static_cast<size_t>(pz_) * Y_.plane;
   auto at = [&](int global_plane) { return buf + static_cast<long long>(global_plane - rlo_) * Y_.plane; };
   const bool lo = rank_ > 0, hi = rank_ + 1 < world_;
-  comm_->exchange(lo ? at(xa_ + pz_) : nullptr, lo ? at(xa_) : nullptr, hi ? at(xb_) : nullptr,
-                  hi ? at(xb_ + pz_) : nullptr, n, stream_);
+  halo_enqueue(buf, lo ? at(xa_ + pz_) : nullptr, lo ? at(xa_) : nullptr, hi ? at(xb_) : nullptr,
+               hi ? at(xb_ + pz_) : nullptr, n);
+}
+
+void Plan::halo_enqueue(const float* buf, const float* send_lo, float* recv_lo, const float* send_hi,
+                        float* recv_hi, size_t n) {
+  wait_halo(buf);  // an earlier exchange of the same buffer (its planes are rewritten now)
+  check_cuda(cudaEventRecord(pass_ev_, stream_), "cudaEventRecord");
+  check_cuda(cudaStreamWaitEvent(comm_stream_, pass_ev_, 0), "cudaStreamWaitEvent");
+  comm_->exchange(send_lo, recv_lo, send_hi, recv_hi, n, comm_stream_);
+  cudaEvent_t& ev = halo_ev_[buf];
+  if (ev == nullptr) check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  check_cuda(cudaEventRecord(ev, comm_stream_), "cudaEventRecord");
+  halo_pending_.insert(buf);
+  if (!halo_overlap_) wait_halo(buf);
+}
+
+void Plan::wait_halo(const float* buf) {
+  if (buf == nullptr || halo_pending_.empty()) return;
+  auto it = halo_pending_.find(buf);
+  if (it == halo_pending_.end()) return;
+  check_cuda(cudaStreamWaitEvent(stream_, halo_ev_[buf], 0), "cudaStreamWaitEvent");
+  halo_pending_.erase(it);
+}
+
+void Plan::drain_halos() {
+  while (!halo_pending_.empty()) wait_halo(*halo_pending_.begin());
 }
 
 // Per-image flags / steps go to the device only when they change (they rarely do), from
@@ -759,6 +833,7 @@ void Plan::d2h_f32_as_f64(double* host, const float* dev, size_t n) {
 }
 
 void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz) {
+  drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   // f64 -> f32 on the host threads, then f32 over PCIe (measured 13.8 vs 15.7 ms for the
   // config-2 batch against the f64 DMA + device conversion)
@@ -787,6 +862,7 @@ void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_of
 }
 
 void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz) {
+  drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
     h2d_staged(staging_, host + b * per, per * 4);
@@ -800,6 +876,7 @@ void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off
 }
 
 void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz) {
+  drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   // Host-side f32 -> f64 conversion halves the PCIe bytes but measured slower than the
   // device conversion + f64 DMA + parallel memcpy (31 vs 19 ms for 16 x 2048^2 on the
@@ -827,6 +904,7 @@ void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_
 }
 
 void Plan::unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_off, int nz) {
+  drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   for (size_t b = 0; b < B_; ++b) {
     check_cuda(launch_unpack_f32(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
@@ -912,6 +990,7 @@ double Plan::estimate_step(size_t power_iters) {
 // they upload the observation (it needs only the PSF and the shape), so the host-side
 // conversion of Y overlaps these device passes.
 void Plan::estimate_launch(size_t power_iters) {
+  drain_halos();
   if (power_iters == 0) fail(NDC_ERR_CONFIG, "estimate_step: power_iters must be positive");
   if (power_iters > static_cast<size_t>(kMaxPowerIters))
     fail(NDC_ERR_UNSUPPORTED, "estimate_step: power_iters too large");
@@ -1051,6 +1130,7 @@ std::vector<size_t> Plan::user_shape(bool y) const {
 // Streams the owned planes of an NDTENSOR file into HBM: each 16 MB pinned chunk is read
 // and checked by the host pool while the previous chunk's H2D is in flight.
 void Plan::load_observation_ndtensor(const std::string& path) {
+  drain_halos();
   const NdtHeader h = read_ndtensor_header(path);
   if (h.ext != user_shape(true))
     fail(NDC_ERR_SHAPE, "load_observation: file shape does not match the plan's observation shape");
@@ -1092,6 +1172,7 @@ void Plan::load_observation_ndtensor(const std::string& path) {
 // Streams the owned estimate planes out: the D2H of chunk k+1 overlaps the host pool's
 // check + pwrite of chunk k.  Sharded ranks write their own planes of one file.
 void Plan::save_estimate_ndtensor(const std::string& path) {
+  drain_halos();
   const std::vector<size_t> ext = user_shape(false);
   const std::string hl = ndtensor_header_line(ext);
   const size_t plane = static_cast<size_t>(my_) * mx_;
@@ -1151,6 +1232,7 @@ void Plan::save_estimate_ndtensor(const std::string& path) {
 }
 
 void Plan::add_gaussian_noise(double mean, double std_dev, uint64_t seed) {
+  drain_halos();
   if (std_dev < 0) fail(NDC_ERR_NUMERIC, "add_gaussian_noise: std_dev must be >= 0");
   const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;
   const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;
@@ -1260,7 +1342,8 @@ void Plan::pg_begin(const ndc_deconv_config& c) {
 // buffers), so the device keeps working while the host makes step k's decision.  When
 // every image did accept (and none stops), the buffers rotate and step k+1 starts at
 // its forward pass; otherwise the speculative pass is discarded (its inputs are
-// unchanged, so it is exact when kept).  One-GPU plans only.
+// unchanged, so it is exact when kept).  z-slab ranks take identical decisions, so they
+// speculate identically.
 size_t Plan::pg_iterate(size_t n) {
   if (!pg_begun_) fail(NDC_ERR_ARGUMENT, "pg_iterate before pg_begin");
   static const bool spec_on = [] {
@@ -1285,19 +1368,20 @@ size_t Plan::pg_iterate(size_t n) {
     if (!spec_ready_) {
       // g = A^T(A x - y) with kkt, trial = max(x - step0 g, 0), changed count (180-191)
       correlate(kAdj, r_, trial_, kEpiPG, g_, x_, nullptr, dstep_, dactive_, true);
+      halo_x(trial_);  // z-slabs: overlaps the forward pass's interior planes
       finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr,
                dactive_);
     }
     spec_ready_ = false;
-    halo_x(trial_);
     // A trial, residual, f_trial (195-197)
     correlate(kFwd, trial_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, dactive_, true);
+    halo_y(rt_);  // z-slabs: r_trial's halo, needed by the next adjoint if it is accepted
     finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kAUX * B_, nullptr, nullptr, dactive_);
     check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
     check_cuda(cudaEventRecord(d2h_ev_, stream_), "cudaEventRecord");
 
     // speculative adjoint of the next step (see above); needs a next step for every image
-    bool spec = spec_on && world_ == 1;
+    bool spec = spec_on;
     for (size_t b = 0; b < B_ && spec; ++b)
       if (act[b] && img_[b].kkt.size() + 1 >= cfg_.max_iters) spec = false;
     if (spec) {
@@ -1307,6 +1391,7 @@ size_t Plan::pg_iterate(size_t n) {
         g2_ = dev_alloc_f(nx);
       }
       correlate(kAdj, rt_, trial2_, kEpiPG, g2_, trial_, nullptr, dstep_, dactive_, true);
+      halo_x(trial2_);
       finalize(partials_per_image(kAdj), kFinMaxSum, dsc_ + kKKT * B_, dsc_ + kCHG * B_, nullptr, dactive_);
     }
     check_cuda(cudaEventSynchronize(d2h_ev_), "cudaEventSynchronize");
@@ -1350,6 +1435,7 @@ size_t Plan::pg_iterate(size_t n) {
       if (nb == 0) break;
       upload_active(bt);
       upload_steps(stp);
+      drain_halos();  // trial_ is rewritten outside correlate()
       check_cuda(launch_pg_trial(x_owned(x_), x_owned(g_), x_owned(trial_), dstep_, dactive_, partials_,
                                  static_cast<int>(B_), X_.geo(xa_n_), kElemBlocks, stream_),
                  "pg_trial launch");
@@ -1357,6 +1443,7 @@ size_t Plan::pg_iterate(size_t n) {
       finalize(kElemBlocks, kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr, dactive_);
       halo_x(trial_);
       correlate(kFwd, trial_, rt_, kEpiResid, nullptr, yobs_, nullptr, nullptr, dactive_, true);
+      halo_y(rt_);
       finalize(partials_per_image(kFwd), kFinHalfSum, dsc_ + kAUX * B_, nullptr, nullptr, dactive_);
       check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_),
                  "D2H");
@@ -1415,9 +1502,8 @@ size_t Plan::pg_iterate(size_t n) {
       for (size_t b = 0; b < B_; ++b)
         if (state[b] != kAccept) {
           copy_image_x(x_, trial_, b);
-          copy_image_y(r_, rt_, b);
+          copy_image_y(r_, rt_, b);  // with its halo planes
         }
-      halo_y(r_);
     }
   }
   active_count = 0;
@@ -1427,11 +1513,13 @@ size_t Plan::pg_iterate(size_t n) {
 }
 
 void Plan::copy_image_x(float* dst, const float* src, size_t b) {
+  drain_halos();
   check_cuda(cudaMemcpyAsync(dst + b * X_.image, src + b * X_.image, X_.image * 4,
                              cudaMemcpyDeviceToDevice, stream_),
              "D2D");
 }
 void Plan::copy_image_y(float* dst, const float* src, size_t b) {
+  drain_halos();
   check_cuda(cudaMemcpyAsync(dst + b * Y_.image, src + b * Y_.image, Y_.image * 4,
                              cudaMemcpyDeviceToDevice, stream_),
              "D2D");
@@ -1512,6 +1600,7 @@ void Plan::set_taps(double scale) {
 //   x'    = x .* A^T ratio, ||x'-x||, ||x||   adjoint pass (290-292)
 // per image, one 3-scalar D2H per iteration.
 void Plan::rl_run(const ndc_rl_config& c) {
+  drain_halos();
   if (c.max_iters == 0) fail(NDC_ERR_CONFIG, "RlConfig: max_iters must be positive");
   if (!(c.tol_rel_change >= 0)) fail(NDC_ERR_CONFIG, "RlConfig: tol_rel_change must be >= 0");
   double hsum = 0.0;

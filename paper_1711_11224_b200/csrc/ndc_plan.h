@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <vector>
@@ -145,6 +146,10 @@ class Plan {
   long long partials_per_image(Dir d) const;
   void halo_x(float* buf);   // fill x-buffer halo planes from neighbours (sharded only)
   void halo_y(float* buf);   // fill y-buffer halo planes from neighbours (sharded only)
+  void halo_enqueue(const float* buf, const float* send_lo, float* recv_lo, const float* send_hi,
+                    float* recv_hi, size_t n);
+  void wait_halo(const float* buf);  // plan stream waits for buf's pending exchange
+  void drain_halos();                // ... for every pending exchange
   void copy_image_x(float* dst, const float* src, size_t b);
   void copy_image_y(float* dst, const float* src, size_t b);
   void sync();
@@ -183,6 +188,12 @@ class Plan {
   int xlo_ = 0, xhi_ = 0;           // x planes held (owned + halo)
   int rlo_ = 0, rhi_ = 0;           // y planes held
   Vol X_, Y_;
+  // halo exchanges run on their own stream, overlapped with the planes that need no halo
+  cudaStream_t comm_stream_ = nullptr;
+  cudaEvent_t pass_ev_ = nullptr;
+  bool halo_overlap_ = true;
+  std::map<const float*, cudaEvent_t> halo_ev_;
+  std::set<const float*> halo_pending_;
 
   // device buffers
   float *x_ = nullptr, *trial_ = nullptr, *g_ = nullptr;

@@ -74,3 +74,46 @@ def test_sharded_rejects_thin_slabs(nd):
     with pytest.raises(nd.UnsupportedError):
         nd.Plan.local(group, 0, (20, 8, 8), h)  # 5-plane slabs < p_z = 10
     group.close()
+
+
+def _run_env(tmp_path, world, step, **env):
+    import os
+    import subprocess
+    import sys
+    out = tmp_path / f"run_{world}_{step}_{'_'.join(f'{k}{v}' for k, v in env.items())}.npz"
+    e = dict(os.environ)
+    e.update({k: str(v) for k, v in env.items()})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, os.path.join(root, "tests", "_sharded_run.py"), str(out), str(world),
+                    str(step)], check=True, env=e, timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("world,step", [(2, 0.0), (3, 0.0), (2, 8.0), (3, 8.0)])
+def test_sharded_overlap_and_speculation_are_exact(nd, tmp_path, world, step):
+    """The halo exchange overlapped with the interior planes (comm stream, per-buffer
+    events) and the speculative next adjoint change only WHEN things run, never what is
+    computed: estimates and traces are bit-identical to the serialised schedule.  World 3
+    on 36 planes gives 12-plane slabs < 2 p_z = 20, where every plane of the middle rank
+    is a boundary plane; initial_step = 8 forces backtracking (acceptance criterion 6's
+    regime), which discards speculative passes."""
+    base = _run_env(tmp_path, world, step, NDC_HALO_OVERLAP=0, NDC_SPECULATE=0)
+    fast = _run_env(tmp_path, world, step)
+    assert np.array_equal(base["x"], fast["x"])
+    assert np.array_equal(base["obj"], fast["obj"]) and np.array_equal(base["kkt"], fast["kkt"])
+    assert int(base["iters"]) == int(fast["iters"]) and str(base["reason"]) == str(fast["reason"])
+    assert int(base["backtracks"]) == int(fast["backtracks"])
+    if step == 8.0:
+        assert int(fast["backtracks"]) > 0  # the backtracking path ran
+
+
+def test_sharded_backtracking_matches_unsharded(nd):
+    from paper_1711_11224_b200 import synth
+    x, y, h = synth.make("c4", shape=(36, 40, 44), n_objects=60)
+    cfg = nd.DeconvConfig(max_iters=12, tol_rel_objective=0.0, initial_step=8.0)
+    xs, reps = run_sharded(nd, 2, y, h, x.shape, cfg)
+    full = nd.deconv_pg(y, h, x.shape, cfg)
+    assert reps[0].extra["backtracks"] == full.extra["backtracks"] > 0
+    assert reps[0].iterations_run == full.iterations_run
+    assert rel_l2(xs, full.estimate) <= 1e-5
+    np.testing.assert_allclose(reps[0].objective_trace, full.objective_trace, rtol=1e-5)

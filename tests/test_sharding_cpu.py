@@ -39,6 +39,49 @@ def _exchange(rank, world, send_lo, send_hi, shape_lo, shape_hi):
     return (None if recv_lo is None else recv_lo.numpy()), (None if recv_hi is None else recv_hi.numpy())
 
 
+def boundary_counts(rank, world, pz):
+    """Planes at the start / end of a pass's computed planes that read the input's halo
+    (ndc_plan.cu correlate(): lo = p_z unless rank 0, hi = p_z unless the last rank)."""
+    return (pz if rank > 0 else 0), (pz if rank < world - 1 else 0)
+
+
+def test_boundary_planes_are_the_halo_planes():
+    """For every slab layout: the computed planes outside the first lo / last hi read only
+    owned input planes (so they may run before the halo exchange), and the planes each
+    neighbour receives as its halo are all among the first lo / last hi (so the exchange
+    can start once those are done) -- forward (x -> y) and adjoint (y -> x)."""
+    from paper_1711_11224_b200 import ndconv as nd
+    for mz in range(1, 41):
+        for pz in range(0, 8):
+            for world in range(1, 6):
+                if world > 1 and mz // world < max(pz, 1):
+                    continue
+                for rank in range(world):
+                    a, b, ya, yb = nd.slab_range(mz, pz, rank, world)
+                    nlo, nhi = boundary_counts(rank, world, pz)
+                    if world == 1:
+                        nlo = nhi = 0
+                    own_y = set(range(ya, yb))
+                    # forward: output plane o reads x planes [o-2p, o] within [0, mz)
+                    for k, o in enumerate(range(ya, yb)):
+                        reads = {z for z in range(o - 2 * pz, o + 1) if 0 <= z < mz}
+                        if nlo <= k < (yb - ya) - nhi:
+                            assert reads <= set(range(a, b)), (mz, pz, world, rank, o)
+                    # adjoint: output x plane o reads y planes [o, o+2p]
+                    for k, o in enumerate(range(a, b)):
+                        reads = set(range(o, o + 2 * pz + 1))
+                        if nlo <= k < (b - a) - nhi:
+                            assert reads <= own_y, (mz, pz, world, rank, o)
+                    # what the neighbours pull: x planes [a, a+p) / [b-p, b), y planes
+                    # [a+p, a+2p) / [b, b+p)
+                    if rank > 0:
+                        assert set(range(a, a + pz)) <= set(range(a, a + nlo))
+                        assert set(range(a + pz, a + 2 * pz)) <= set(range(ya, ya + nlo))
+                    if rank < world - 1:
+                        assert set(range(b - pz, b)) <= set(range(b - nhi, b))
+                        assert set(range(b, b + pz)) <= set(range(yb - nhi, yb))
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -54,6 +97,10 @@ def _worker(rank, world, port, q):
         x = g.uniform(-1, 1, (mz, my, mx))
         y = g.uniform(-1, 1, (mz + 4, my + 2, mx + 2))
         a, b, ya, yb = nd.slab_range(mz, pz, rank, world)
+        # overlapped schedule (ndc_plan.cu correlate()): the planes that need no halo are
+        # computed from the owned planes alone BEFORE the exchange
+        nlo, nhi = boundary_counts(rank, world, pz)
+        interior_fwd = orc.conv_full(x[a:b], h)[ya + nlo - a: yb - nhi - a]
         # forward: hold x planes [max(0,a-p), min(mz,b+p)) via halos
         lo, hi = _exchange(rank, world, x[a:a + pz], x[b - pz:b], (pz, my, mx), (pz, my, mx))
         parts = [p for p in (lo, x[a:b], hi) if p is not None]
@@ -61,6 +108,7 @@ def _worker(rank, world, port, q):
         x0 = a - (pz if lo is not None else 0)
         yl = orc.conv_full(xl, h)                      # local full conv of the slab
         own_fwd = yl[ya - x0: yb - x0]                  # owned y planes
+        assert np.array_equal(own_fwd[nlo:own_fwd.shape[0] - nhi], interior_fwd)
         # adjoint: hold y planes [a, b+2p): own [ya, yb) + halos from neighbours
         lo, hi = _exchange(rank, world, y[a + pz:a + 2 * pz], y[b:b + pz], (pz,) + y.shape[1:],
                            (pz,) + y.shape[1:])
