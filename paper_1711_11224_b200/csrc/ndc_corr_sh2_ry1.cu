@@ -7,7 +7,7 @@ namespace ndc {
 
 cudaError_t launch_correlate_sh2_ry1(int kx, const CUtensorMap& map, const CorrGeom& g,
                                       const CorrArgs& a, const TapBlock& taps, int batch,
-                                      int nz_out, cudaStream_t s) {
+                                      int nz_out, cudaStream_t s, cudaStream_t s_edge) {
   using namespace corr;
   NDC_KX_SWITCH(2, 1)
 }

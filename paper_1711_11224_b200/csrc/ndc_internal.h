@@ -95,15 +95,17 @@ __host__ __device__ constexpr int tap_pitch(int kx) { return (kx + 1) & ~1; }
 
 // Launch the correlation kernel for one tap chunk; sh (0 or 2) is the register-window
 // shift that keeps the TMA tile start 16-byte aligned, ry (1 or 2) the output rows per
-// thread (tile height 64*ry).
+// thread (tile height 64*ry).  The full tiles run on stream s, the partial edge tiles
+// (a second launch) on s_edge, which may be a different stream so the edge CTAs fill the
+// SMs freed by the full-tile launch's last wave.
 cudaError_t launch_correlate(int kx, int sh, int ry, const CUtensorMap& map, const CorrGeom& g,
                              const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
-                             cudaStream_t s);
+                             cudaStream_t s, cudaStream_t s_edge);
 #define NDC_DECL_CORR(SH, RY)                                                               \
   cudaError_t launch_correlate_sh##SH##_ry##RY(int kx, const CUtensorMap& map,             \
                                                const CorrGeom& g, const CorrArgs& a,       \
                                                const TapBlock& taps, int batch, int nz_out, \
-                                               cudaStream_t s);
+                                               cudaStream_t s, cudaStream_t s_edge);
 NDC_DECL_CORR(0, 1)
 NDC_DECL_CORR(0, 2)
 NDC_DECL_CORR(2, 1)

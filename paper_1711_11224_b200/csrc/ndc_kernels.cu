@@ -273,11 +273,11 @@ size_t correlate_smem_bytes(const CorrGeom& g) {
 
 cudaError_t launch_correlate(int kx, int sh, int ry, const CUtensorMap& map, const CorrGeom& g,
                              const CorrArgs& a, const TapBlock& taps, int batch, int nz_out,
-                             cudaStream_t s) {
-  if (sh == 0 && ry == 1) return launch_correlate_sh0_ry1(kx, map, g, a, taps, batch, nz_out, s);
-  if (sh == 0 && ry == 2) return launch_correlate_sh0_ry2(kx, map, g, a, taps, batch, nz_out, s);
-  if (sh == 2 && ry == 1) return launch_correlate_sh2_ry1(kx, map, g, a, taps, batch, nz_out, s);
-  if (sh == 2 && ry == 2) return launch_correlate_sh2_ry2(kx, map, g, a, taps, batch, nz_out, s);
+                             cudaStream_t s, cudaStream_t s_edge) {
+  if (sh == 0 && ry == 1) return launch_correlate_sh0_ry1(kx, map, g, a, taps, batch, nz_out, s, s_edge);
+  if (sh == 0 && ry == 2) return launch_correlate_sh0_ry2(kx, map, g, a, taps, batch, nz_out, s, s_edge);
+  if (sh == 2 && ry == 1) return launch_correlate_sh2_ry1(kx, map, g, a, taps, batch, nz_out, s, s_edge);
+  if (sh == 2 && ry == 2) return launch_correlate_sh2_ry2(kx, map, g, a, taps, batch, nz_out, s, s_edge);
   return cudaErrorInvalidValue;
 }
 

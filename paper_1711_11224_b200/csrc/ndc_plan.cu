@@ -119,7 +119,11 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     // small PSFs are HBM-bound: 64-row tiles at 4 CTAs / SM keep more loads in flight
     if (KX_ <= kSmallMaxKX) ry_ = 1;
   }
-  if (const char* e = std::getenv("NDC_TUNE_RY")) ry_ = std::atoi(e) == 1 ? 1 : ry_;  // tuning hook
+  if (const char* e = std::getenv("NDC_TUNE_RY")) {  // tuning hook
+    const int v = std::atoi(e);
+    if (v == 1) ry_ = 1;
+    if (v == 2 && 2 * kTileY + KY_ - 1 <= kMaxRows) ry_ = 2;
+  }
   kcy_ = std::min(KY_, kMaxRows - kTileY * ry_ + 1);  // staged rows 64*ry + kcy - 1 <= TMA box limit
 
   if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
@@ -178,6 +182,9 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   if (prop.major != 10)
     fail(NDC_ERR_NO_DEVICE, std::string("ndconv_b200: built for sm_100a, device is ") + prop.name);
   check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  check_cuda(cudaStreamCreateWithFlags(&edge_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  check_cuda(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "cudaEventCreate");
+  check_cuda(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming), "cudaEventCreate");
   if (world_ > 1) {
     check_cuda(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     check_cuda(cudaEventCreateWithFlags(&pass_ev_, cudaEventDisableTiming), "cudaEventCreate");
@@ -190,6 +197,7 @@ Plan::~Plan() {
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);  // halo sends read plan buffers
+  if (edge_stream_) cudaStreamSynchronize(edge_stream_);
   for (auto& e : ev_pool_) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -207,6 +215,9 @@ Plan::~Plan() {
   for (auto& e : halo_ev_)
     if (e.second) cudaEventDestroy(e.second);
   if (pass_ev_) cudaEventDestroy(pass_ev_);
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+  if (join_ev_) cudaEventDestroy(join_ev_);
+  if (edge_stream_) cudaStreamDestroy(edge_stream_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
   if (hsc_) small_pinned_put(small_bytes_, hsc_);
   if (up_ev_) cudaEventDestroy(up_ev_);
@@ -574,7 +585,26 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   static thread_local TapBlock tb;
   // One launch per tap chunk over the computed planes [z_base, z_base + nz), skipping
   // `gap` planes once `gap_at` planes are done.
+  // Partial edge tiles run on the side stream (fork / join around the whole pass), so
+  // their CTAs fill the SMs the full-tile launch frees in its last wave; each stream keeps
+  // its tap chunks in order, and the two touch disjoint output tiles.
+  const bool side = g.tiles_x * g.tiles_y > g.full_tx * g.full_ty && g.full_tx * g.full_ty > 0;
   auto run_chunks = [&](int z_base, int nz, int gap_at, int gap) {
+    size_t ev = 0;
+    if (timing_) {
+      if (ev_used_ == ev_pool_.size()) {
+        cudaEvent_t e0, e1;
+        check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
+        check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+        ev_pool_.emplace_back(e0, e1);
+      }
+      ev = ev_used_++;
+      check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
+    }
+    if (side) {
+      check_cuda(cudaEventRecord(fork_ev_, stream_), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(edge_stream_, fork_ev_, 0), "cudaStreamWaitEvent");
+    }
     for (size_t c = 0; c < chunks.size(); ++c) {
       const Chunk& ch = chunks[c];
       g.KY = ch.cy;
@@ -618,25 +648,19 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
           }
       }
       const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
-      size_t ev = 0;
-      if (timing_) {
-        if (ev_used_ == ev_pool_.size()) {
-          cudaEvent_t e0, e1;
-          check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
-          check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
-          ev_pool_.emplace_back(e0, e1);
-        }
-        ev = ev_used_++;
-        check_cuda(cudaEventRecord(ev_pool_[ev].first, stream_), "cudaEventRecord");
-      }
-      check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz, stream_),
+      check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz, stream_,
+                                  side ? edge_stream_ : stream_),
                  "correlate launch");
-      if (timing_) {
-        check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
-        ev_pending_.emplace_back(fwd ? 0 : 1, ev);
-      }
       st_[fwd ? 0 : 1].launches++;
       st_[2].launches++;
+    }
+    if (side) {
+      check_cuda(cudaEventRecord(join_ev_, edge_stream_), "cudaEventRecord");
+      check_cuda(cudaStreamWaitEvent(stream_, join_ev_, 0), "cudaStreamWaitEvent");
+    }
+    if (timing_) {
+      check_cuda(cudaEventRecord(ev_pool_[ev].second, stream_), "cudaEventRecord");
+      ev_pending_.emplace_back(fwd ? 0 : 1, ev);
     }
   };
   // Outputs still being sent to a neighbour, or halo planes still arriving, must not be

@@ -190,6 +190,9 @@ class Plan {
   Vol X_, Y_;
   // halo exchanges run on their own stream, overlapped with the planes that need no halo
   cudaStream_t comm_stream_ = nullptr;
+  // partial edge tiles of a pass run on a side stream (fork / join per pass)
+  cudaStream_t edge_stream_ = nullptr;
+  cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
   cudaEvent_t pass_ev_ = nullptr;
   bool halo_overlap_ = true;
   std::map<const float*, cudaEvent_t> halo_ev_;
