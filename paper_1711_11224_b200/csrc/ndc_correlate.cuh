@@ -429,15 +429,42 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // warp-uniform (keeps the tap loads on the uniform datapath under those branches)
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   int wx = warp & 3, wy = warp >> 2, pw = warp, phase = 0, nph = 1, P = 8;
+  // Per-lane placement: output row offset within the tile and column offset of the lane's
+  // 16-column strip.  Normally a warp is 32 consecutive rows of one strip; in a COMPACT
+  // edge tile (<= 16 rows left: the bottom tile row of e.g. config 3's 270-row or config
+  // 4's 1032-row forward output) a warp is LR = 8 or 16 rows x 32/LR strips, so its lanes
+  // are not idle on rows past the extent.  A quarter-warp is still 8 consecutive rows of
+  // one strip (bank-conflict-free loads).
+  int lane_row = 0, lane_col = 0;
+  bool compact = false;
   if (EDGE) {
     const int S = min(4, (g.out_ex - tx0 + kRX - 1) / kRX);
-    const int R = min(2, (g.out_ey - ty0 + 32 * RY - 1) / (32 * RY));
-    P = S * R;
-    pw = __shfl_sync(0xffffffffu, warp % P, 0);
-    phase = __shfl_sync(0xffffffffu, warp / P, 0);
-    nph = (7 - pw) / P + 1;
-    wx = __shfl_sync(0xffffffffu, pw % S, 0);
-    wy = __shfl_sync(0xffffffffu, pw / S, 0);
+    const int rows_left = g.out_ey - ty0;
+    compact = rows_left <= 16;
+    if (compact) {
+      const int LR = rows_left <= 8 ? 8 : 16;
+      const int spw = 32 / LR;             // strips per warp
+      P = (S + spw - 1) / spw;             // warp units
+      pw = __shfl_sync(0xffffffffu, warp % P, 0);
+      phase = __shfl_sync(0xffffffffu, warp / P, 0);
+      nph = (7 - pw) / P + 1;
+      wx = 0;
+      wy = 0;
+      lane_row = lane % LR;
+      lane_col = (pw * spw + lane / LR) * kRX;
+    } else {
+      const int R = min(2, (rows_left + 32 * RY - 1) / (32 * RY));
+      P = S * R;
+      pw = __shfl_sync(0xffffffffu, warp % P, 0);
+      phase = __shfl_sync(0xffffffffu, warp / P, 0);
+      nph = (7 - pw) / P + 1;
+      wx = __shfl_sync(0xffffffffu, pw % S, 0);
+      wy = __shfl_sync(0xffffffffu, pw / S, 0);
+    }
+  }
+  if (!compact) {
+    lane_row = wy * (32 * RY) + lane;
+    lane_col = wx * kRX;
   }
 
   // Tap slices whose input plane iz = oz + kz + off_z exists (out-of-range planes are
@@ -469,7 +496,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // Small PSFs: prefetch the epilogue's aux_in strip (Y or x) into shared memory now,
   // so it arrives during the FFMA loop instead of stalling the epilogue.
   const float* wpre = nullptr;
-  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0) {
+  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
+      !compact) {
     float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
                  warp * (RY * 32 * kRX);
     const int ox0 = tx0 + wx * kRX;
@@ -497,7 +525,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
 #pragma unroll
     for (int c = 0; c < kRX; ++c) acc[j][c] = 0.f;
 
-  const int row_l = wy * (32 * RY) + lane;
   // Rows blocks / column strips entirely outside the output (the last tiles of an
   // extent that is not a tile multiple) skip their FFMAs; the test is warp-uniform.
   int nrun = 0;
@@ -505,11 +532,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   for (int j = 0; j < RY; ++j)
     if (ty0 + wy * (32 * RY) + 32 * j < g.out_ey) nrun = j + 1;
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
+  if (compact) nrun = 1;  // rows 0..15 of block 0 only; inactive lanes are masked at the end
   for (int i = 0; i < n; ++i) {
     const int s = i % g.stages;
     mbar_wait(&bars[s], static_cast<uint32_t>((i / g.stages) & 1));
     const float* base =
-        reinterpret_cast<const float*>(smem_raw + s * sbytes) + row_l * g.pitch_s + wx * kRX;
+        reinterpret_cast<const float*>(smem_raw + s * sbytes) + lane_row * g.pitch_s + lane_col;
     const float* trow = taps.t + (kzA + i - g.kz0) * g.KY * tap_pitch(KX);
     if (nrun == RY)
       accumulate_rows<KX, SH, RY, RY, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
@@ -561,9 +589,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // ---- epilogue (one instantiation per mode: the dispatch happens once per tile) --------
   float* wst = reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
   double p0 = 0.0, p1 = 0.0;
-#define NDC_EPI(M) \
-  epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, wst, \
-                                             wpre, p0, p1)
+  // (compact edge tiles: per-lane row / strip, so the lane-per-row direct epilogue; its
+  // row is wrow0 + lane, hence the per-lane wrow0)
+#define NDC_EPI(M)                                                                                      \
+  if (compact)                                                                                        \
+    epilogue_tile<M, RY, false>(g, a, b, oz, tx0 + lane_col, ty0 + lane_row - lane, lane, acc, wst, nullptr, \
+                                p0, p1);                                                                \
+  else                                                                                                \
+    epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, \
+                                               wst, wpre, p0, p1)
   switch (phase != 0 ? -2 : g.final_chunk ? g.mode : -1) {  // -2: folded into a phase-0 warp
     case kEpiStore: NDC_EPI(kEpiStore); break;
     case kEpiResid: NDC_EPI(kEpiResid); break;
@@ -595,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
 
 template <int KX, int SH, int RY>
 cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs& a,
-                      const TapBlock& taps, int batch, int nz_out, cudaStream_t s) {
+                      const TapBlock& taps, int batch, int nz_out, cudaStream_t s, cudaStream_t s_edge) {
   // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
   const size_t smem = correlate_smem_bytes(g) +
                       ((KX <= NDC_STAGED_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
@@ -617,29 +651,29 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
   }
   if (n_edge > 0)
-    correlate_kernel<KX, SH, RY, true><<<dim3(n_edge, nz_out, batch), kThreads, smem, s>>>(map, g, a, taps);
+    correlate_kernel<KX, SH, RY, true><<<dim3(n_edge, nz_out, batch), kThreads, smem, s_edge>>>(map, g, a, taps);
   return cudaGetLastError();
 }
 
 #define NDC_KX_SWITCH(SH, RY)                                              \
   switch (kx) {                                                            \
-    case 1: return launch_kx<1, SH, RY>(map, g, a, taps, batch, nz_out, s);   \
-    case 3: return launch_kx<3, SH, RY>(map, g, a, taps, batch, nz_out, s);   \
-    case 5: return launch_kx<5, SH, RY>(map, g, a, taps, batch, nz_out, s);   \
-    case 7: return launch_kx<7, SH, RY>(map, g, a, taps, batch, nz_out, s);   \
-    case 9: return launch_kx<9, SH, RY>(map, g, a, taps, batch, nz_out, s);   \
-    case 11: return launch_kx<11, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 13: return launch_kx<13, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 15: return launch_kx<15, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 17: return launch_kx<17, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 19: return launch_kx<19, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 21: return launch_kx<21, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 23: return launch_kx<23, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 25: return launch_kx<25, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 27: return launch_kx<27, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 29: return launch_kx<29, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 31: return launch_kx<31, SH, RY>(map, g, a, taps, batch, nz_out, s); \
-    case 33: return launch_kx<33, SH, RY>(map, g, a, taps, batch, nz_out, s); \
+    case 1: return launch_kx<1, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge);   \
+    case 3: return launch_kx<3, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge);   \
+    case 5: return launch_kx<5, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge);   \
+    case 7: return launch_kx<7, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge);   \
+    case 9: return launch_kx<9, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge);   \
+    case 11: return launch_kx<11, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 13: return launch_kx<13, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 15: return launch_kx<15, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 17: return launch_kx<17, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 19: return launch_kx<19, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 21: return launch_kx<21, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 23: return launch_kx<23, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 25: return launch_kx<25, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 27: return launch_kx<27, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 29: return launch_kx<29, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 31: return launch_kx<31, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
+    case 33: return launch_kx<33, SH, RY>(map, g, a, taps, batch, nz_out, s, s_edge); \
     default: return cudaErrorInvalidValue;                                 \
   }
 

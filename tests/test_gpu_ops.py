@@ -191,3 +191,30 @@ def test_batched_float32_operators(nd, oracle_c):
         g = nd.adjoint_apply_batch(r, h, xs[1:])
         for b in range(xs[0]):
             assert rel_l2(g[b], oracle_c.adjoint_apply(r[b].astype(np.float64), h, xs[1:])) <= 1e-5
+
+
+@pytest.mark.parametrize("xs,hs", [((124, 100), (15, 15)), ((231, 90), (31, 31)), ((125, 200), (9, 9)),
+                                   ((6, 64, 64), (5, 15, 15)), ((6, 128, 100), (5, 9, 9)),
+                                   ((3, 50, 64), (3, 15, 7))])
+def test_edge_tiles_few_rows(nd, oracle_c, xs, hs):
+    """Output extents that leave 1-16 rows in the last tile row (config 3's 270-row and
+    config 4's 1032-row forward outputs are of this kind) run the edge kernel's compact
+    lane mapping (8 or 16 rows x 4 or 2 strips per warp); every element of forward and
+    adjoint, and a short PG run (fused epilogues + reductions), against the oracle."""
+    rng = np.random.default_rng(sum(xs) + sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    y_ref = oracle_c.conv_full(x, h)
+    y = nd.conv_full(x, h)
+    assert np.max(np.abs(y - y_ref)) <= 1e-5 * np.max(np.abs(y_ref))
+    r = rng.uniform(-1, 1, y_ref.shape)
+    a_ref = oracle_c.adjoint_apply(r, h, xs)
+    assert np.max(np.abs(nd.adjoint_apply(r, h, xs) - a_ref)) <= 1e-5 * np.max(np.abs(a_ref))
+    yo = y_ref + rng.uniform(0, 1e-3, y_ref.shape)
+    cfg = nd.DeconvConfig(max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    got = nd.deconv_pg(yo, h, xs, cfg)
+    want = oracle_c.deconv_pg(yo, h, xs, max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    assert got.iterations_run == want.iterations_run
+    assert rel_l2(got.estimate, want.estimate) <= 1e-4
+    np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
