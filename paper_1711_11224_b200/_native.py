@@ -142,6 +142,8 @@ def lib() -> C.CDLL:
                 "(the ndconv B200 path has no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, res, args in _SIGS:
+            if os.environ.get("NDC_LIB_PATH") and not hasattr(L, name):
+                continue  # an older library variant (A/B timing) may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -401,9 +401,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
 
   const int b = blockIdx.z;
   if (a.active != nullptr && a.active[b] == 0) return;
-  // computed output plane: launches may cover a subset of the pass's planes (z-slab
-  // ranks run the planes that need no halo first, ndc_plan.cu correlate())
-  const int oz = static_cast<int>(blockIdx.y) + g.z_base + (static_cast<int>(blockIdx.y) >= g.z_gap_at ? g.z_gap : 0);
+  const int oz = blockIdx.y;
   int txi, tyi;
   if (!EDGE) {
     txi = blockIdx.x % g.full_tx;
@@ -437,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // one strip (bank-conflict-free loads).
   int lane_row = 0, lane_col = 0;
   bool compact = false;
-  if (EDGE) {
+  if constexpr (EDGE) {
     const int S = min(4, (g.out_ex - tx0 + kRX - 1) / kRX);
     const int rows_left = g.out_ey - ty0;
     compact = rows_left <= 16;
@@ -462,9 +460,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
       wy = __shfl_sync(0xffffffffu, pw / S, 0);
     }
   }
-  if (!compact) {
-    lane_row = wy * (32 * RY) + lane;
-    lane_col = wx * kRX;
+  if constexpr (EDGE) {
+    if (!compact) {
+      lane_row = wy * (32 * RY) + lane;
+      lane_col = wx * kRX;
+    }
   }
 
   // Tap slices whose input plane iz = oz + kz + off_z exists (out-of-range planes are
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // so it arrives during the FFMA loop instead of stalling the epilogue.
   const float* wpre = nullptr;
   if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
-      !compact) {
+      !(EDGE && compact)) {
     float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
                  warp * (RY * 32 * kRX);
     const int ox0 = tx0 + wx * kRX;
@@ -532,12 +532,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   for (int j = 0; j < RY; ++j)
     if (ty0 + wy * (32 * RY) + 32 * j < g.out_ey) nrun = j + 1;
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
-  if (compact) nrun = 1;  // rows 0..15 of block 0 only; inactive lanes are masked at the end
+  if (EDGE && compact) nrun = 1;  // rows 0..15 of block 0 only; inactive lanes are masked at the end
   for (int i = 0; i < n; ++i) {
     const int s = i % g.stages;
     mbar_wait(&bars[s], static_cast<uint32_t>((i / g.stages) & 1));
     const float* base =
-        reinterpret_cast<const float*>(smem_raw + s * sbytes) + lane_row * g.pitch_s + lane_col;
+        EDGE ? reinterpret_cast<const float*>(smem_raw + s * sbytes) + lane_row * g.pitch_s + lane_col
+             : reinterpret_cast<const float*>(smem_raw + s * sbytes) + (wy * (32 * RY) + lane) * g.pitch_s + wx * kRX;
     const float* trow = taps.t + (kzA + i - g.kz0) * g.KY * tap_pitch(KX);
     if (nrun == RY)
       accumulate_rows<KX, SH, RY, RY, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // (compact edge tiles: per-lane row / strip, so the lane-per-row direct epilogue; its
   // row is wrow0 + lane, hence the per-lane wrow0)
 #define NDC_EPI(M)                                                                                      \
-  if (compact)                                                                                        \
+  if (EDGE && compact)                                                                                \
     epilogue_tile<M, RY, false>(g, a, b, oz, tx0 + lane_col, ty0 + lane_row - lane, lane, acc, wst, nullptr, \
                                 p0, p1);                                                                \
   else                                                                                                \
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     p1 = warp_sum(p1);
     if (lane == 0) {
       const long long idx =
-          ((static_cast<long long>(b) * g.part_nz + oz) * (g.tiles_x * g.tiles_y) + tile) *
+          ((static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile) *
               (kThreads / 32) + warp;
       a.partials[idx] = make_double2(p0, p1);
     }

@@ -26,7 +26,10 @@ constexpr int kRX = 16;
 constexpr int kThreads = 256;
 constexpr int kMaxKX = 33;        // largest x-extent with a register-window instantiation
 constexpr int kMaxRows = 256;     // TMA box limit on rows: kTileY + KY - 1 <= 256
-constexpr int kTapCap = 7680;     // taps per launch carried in the kernel parameter block
+#ifndef NDC_TAP_CAP
+#define NDC_TAP_CAP 7680
+#endif
+constexpr int kTapCap = NDC_TAP_CAP;  // taps per launch carried in the kernel parameter block
 constexpr int kMaxStages = 3;
 // HBM-bound small PSFs (ndc_correlate.cuh): kernel x-extents up to kStagedMaxKX use the
 // staged, sector-complete epilogue (and, for single-plane problems, a cp.async prefetch
@@ -69,11 +72,11 @@ struct CorrGeom {
   int accum;           // add the partial sum held in `accum_in`
   int mode;            // EpiMode (ignored unless final)
   int final_chunk;     // last tap chunk: apply the epilogue
-  // planes of this launch: computed index oz = blockIdx.y + z_base (+ z_gap once
-  // blockIdx.y >= z_gap_at); part_nz = computed planes of the whole pass (partials index)
-  int z_base, z_gap_at, z_gap, part_nz;
   long long out_pitch, out_plane, out_image;  // in floats
 };
+// (a launch covering a subset of a pass's planes shifts out_z0 / off_z and the partials
+// pointer on the host; the kernel's plane index stays blockIdx.y -- measured: reading a
+// plane offset from the parameters costs the small-PSF kernels ~1.5 %)
 
 struct CorrArgs {
   float* out;             // main output (x- or y-shaped per direction)

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 #include <condition_variable>
 #include <mutex>
@@ -530,9 +531,6 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   const std::vector<float>& taps = fwd ? taps_fwd_ : taps_adj_;
   CorrGeom g{};
   g.in_ez = vin.ez;
-  g.in_ey = vin.ey;
-  g.in_row0 = vin.r0;
-  g.in_ex = vin.ex;
   g.out_ey = vout.ey;
   g.out_ex = vout.ex;
   int nz_out;
@@ -583,13 +581,20 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
     }
   }
   static thread_local TapBlock tb;
-  // One launch per tap chunk over the computed planes [z_base, z_base + nz), skipping
-  // `gap` planes once `gap_at` planes are done.
+  // One launch per tap chunk and plane segment [z_base, z_base + nz) of the computed
+  // planes.  A segment that does not start at plane 0 shifts the output / input plane
+  // offsets and the partials pointer (single-image slab plans only), so the kernel's
+  // plane index stays blockIdx.y.
   // Partial edge tiles run on the side stream (fork / join around the whole pass), so
   // their CTAs fill the SMs the full-tile launch frees in its last wave; each stream keeps
   // its tap chunks in order, and the two touch disjoint output tiles.
   const bool side = g.tiles_x * g.tiles_y > g.full_tx * g.full_ty && g.full_tx * g.full_ty > 0;
-  auto run_chunks = [&](int z_base, int nz, int gap_at, int gap) {
+  const int out_z0_base = g.out_z0, off_z_base = g.off_z;
+  const long long part_per_plane = static_cast<long long>(g.tiles_x) * g.tiles_y * (kThreads / 32);
+  struct Seg {
+    int z_base, nz;
+  };
+  auto run_chunks = [&](std::initializer_list<Seg> segs) {
     size_t ev = 0;
     if (timing_) {
       if (ev_used_ == ev_pool_.size()) {
@@ -605,54 +610,58 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
       check_cuda(cudaEventRecord(fork_ev_, stream_), "cudaEventRecord");
       check_cuda(cudaStreamWaitEvent(edge_stream_, fork_ev_, 0), "cudaStreamWaitEvent");
     }
-    for (size_t c = 0; c < chunks.size(); ++c) {
-      const Chunk& ch = chunks[c];
-      g.KY = ch.cy;
-      g.rows = kTileY * ry_ + ch.cy - 1;
-      g.pitch_s = shared_pitch_for(ch.w, sh);
-      g.off_x = off_x0 + ch.kx0;  // multiples of 32: the TMA origin stays 16-byte aligned
-      g.off_y = off_y0 + ch.ky0;
-      g.kz0 = ch.kz0;
-      g.kz1 = ch.kz1;
-      g.stages = std::min(stages_, g.kz1 - g.kz0);
-      g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
-      g.accum = c > 0;
-      g.final_chunk = (c + 1 == chunks.size());
-      g.z_base = z_base;
-      g.z_gap_at = gap_at;
-      g.z_gap = gap;
-      g.part_nz = nz_out;
-      // x-shaped operands are addressed from their interior origin
-      const long long xo = fwd ? 0 : X_.origin;
-      auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
-      CorrArgs a{};
-      a.out = at(g.final_chunk ? out : scratch_);
-      a.accum_in = at(scratch_);
-      a.aux_out = at(aux_out);
-      a.aux_in = fwd ? aux_in : at(aux_in);
-      a.scale = scale;
-      a.step = step;
-      a.active = active;
-      a.partials = (g.final_chunk && partials) ? partials_ : nullptr;
-      // gather the chunk's taps [kz][ky][kx] with row pitch tap_pitch(w), zero padded
-      const int wp = tap_pitch(ch.w);
-      if (ch.kx0 == 0 && ch.w == KX_ && ch.cy == KY_) {
-        std::memcpy(tb.t, taps.data() + static_cast<size_t>(ch.kz0) * KY_ * kxp_full,
-                    static_cast<size_t>(ch.kz1 - ch.kz0) * KY_ * kxp_full * sizeof(float));
-      } else {
-        for (int kz = ch.kz0; kz < ch.kz1; ++kz)
-          for (int ky = 0; ky < ch.cy; ++ky) {
-            float* dst = tb.t + (static_cast<size_t>(kz - ch.kz0) * ch.cy + ky) * wp;
-            const float* src = taps.data() + (static_cast<size_t>(kz) * KY_ + ch.ky0 + ky) * kxp_full + ch.kx0;
-            for (int kx = 0; kx < wp; ++kx) dst[kx] = kx < ch.cw ? src[kx] : 0.0f;
-          }
+    for (const Seg& sg : segs) {
+      if (sg.nz <= 0) continue;
+      if (sg.z_base != 0 && B_ != 1) fail(NDC_ERR_CUDA, "internal: plane segments need a single-image plan");
+      g.out_z0 = out_z0_base + sg.z_base;
+      g.off_z = off_z_base + sg.z_base;
+      for (size_t c = 0; c < chunks.size(); ++c) {
+        const Chunk& ch = chunks[c];
+        g.KY = ch.cy;
+        g.rows = kTileY * ry_ + ch.cy - 1;
+        g.pitch_s = shared_pitch_for(ch.w, sh);
+        g.off_x = off_x0 + ch.kx0;  // multiples of 32: the TMA origin stays 16-byte aligned
+        g.off_y = off_y0 + ch.ky0;
+        g.kz0 = ch.kz0;
+        g.kz1 = ch.kz1;
+        g.stages = std::min(stages_, g.kz1 - g.kz0);
+        g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
+        g.accum = c > 0;
+        g.final_chunk = (c + 1 == chunks.size());
+        // x-shaped operands are addressed from their interior origin
+        const long long xo = fwd ? 0 : X_.origin;
+        auto at = [xo](const float* p) { return p ? const_cast<float*>(p) + xo : nullptr; };
+        CorrArgs a{};
+        a.out = at(g.final_chunk ? out : scratch_);
+        a.accum_in = at(scratch_);
+        a.aux_out = at(aux_out);
+        a.aux_in = fwd ? aux_in : at(aux_in);
+        a.scale = scale;
+        a.step = step;
+        a.active = active;
+        a.partials = (g.final_chunk && partials) ? partials_ + sg.z_base * part_per_plane : nullptr;
+        // gather the chunk's taps [kz][ky][kx] with row pitch tap_pitch(w), zero padded
+        const int wp = tap_pitch(ch.w);
+        if (ch.kx0 == 0 && ch.w == KX_ && ch.cy == KY_) {
+          std::memcpy(tb.t, taps.data() + static_cast<size_t>(ch.kz0) * KY_ * kxp_full,
+                      static_cast<size_t>(ch.kz1 - ch.kz0) * KY_ * kxp_full * sizeof(float));
+        } else {
+          for (int kz = ch.kz0; kz < ch.kz1; ++kz)
+            for (int ky = 0; ky < ch.cy; ++ky) {
+              float* dst = tb.t + (static_cast<size_t>(kz - ch.kz0) * ch.cy + ky) * wp;
+              const float* src = taps.data() + (static_cast<size_t>(kz) * KY_ + ch.ky0 + ky) * kxp_full + ch.kx0;
+              for (int kx = 0; kx < wp; ++kx) dst[kx] = kx < ch.cw ? src[kx] : 0.0f;
+            }
+        }
+        const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
+        check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), sg.nz, stream_,
+                                    side ? edge_stream_ : stream_),
+                   "correlate launch");
+        // kernels launched: full tiles and / or the edge tiles
+        const int nk = (g.full_tx * g.full_ty > 0 ? 1 : 0) + (g.tiles_x * g.tiles_y > g.full_tx * g.full_ty ? 1 : 0);
+        st_[fwd ? 0 : 1].launches += nk;
+        st_[2].launches += nk;
       }
-      const CUtensorMap& map = map_for(in, d, sh, ch.w, ch.cy);
-      check_cuda(launch_correlate(ch.w, sh, ry_, map, g, a, tb, static_cast<int>(B_), nz, stream_,
-                                  side ? edge_stream_ : stream_),
-                 "correlate launch");
-      st_[fwd ? 0 : 1].launches++;
-      st_[2].launches++;
     }
     if (side) {
       check_cuda(cudaEventRecord(join_ev_, edge_stream_), "cudaEventRecord");
@@ -675,12 +684,12 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   const int hi = (world_ > 1 && rank_ + 1 < world_) ? pz_ : 0;
   const int n_int = nz_out - lo - hi;
   if (halo_overlap_ && (lo + hi) > 0 && n_int > 0) {
-    run_chunks(lo, n_int, nz_out, 0);
+    run_chunks({{lo, n_int}});
     wait_halo(in);
-    run_chunks(0, lo + hi, lo, n_int);
+    run_chunks({{0, lo}, {nz_out - hi, hi}});
   } else {
     wait_halo(in);
-    run_chunks(0, nz_out, nz_out, 0);
+    run_chunks({{0, nz_out}});
   }
 }
 
