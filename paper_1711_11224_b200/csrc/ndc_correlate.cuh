@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "ndc_internal.h"
@@ -328,9 +329,76 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
   }
 }
 
+// Packed FP32 (sm_100 FFMA2): one instruction does two FMAs, so the FMA pipe -- not the
+// issue slot -- bounds the tap loop, and the window LDS / tap LDCU / loop control issue in
+// the slots FFMA2 leaves free (measured 73.3 vs 70.2 TFLOP/s for FFMA on a register-
+// blocked loop, tools/probe/f2.cu).  A lane's 16 outputs are column pairs, and the tap is
+// a broadcast scalar operand (`FFMA2 R, R, UR.F32, R`: no tap shuffling):
+//   even tap kx: pairs (c, c+1), c = 0, 2, .., 14 -- window pair (c+kx, c+kx+1) starts at
+//                an even register (a 64-bit aligned pair);
+//   odd tap kx:  pairs (c, c+1), c = 1, 3, .., 13, into a second accumulator set, plus
+//                scalar FFMAs for columns 0 and 15 (again even-aligned window pairs).
+// Exactly 16*KX MACs per row window (8 FFMA2 per even tap, 7 FFMA2 + 2 FFMA per odd tap);
+// the two sets are added once after the tap loop.
+//
+// Where it pays (tools/kbench.py, one B200, 2048^2 x 16 batch with N x N PSFs, both
+// passes): N = 7..17 +8..26 %, 21 +3..5 %, 25..31 neutral, 33 -1 %; 3-D config 3
+// (15 x 15 rows) +2 % forward; 3-D config 4 (9 x 9 rows) -8 %.  So: packed for
+// 11 <= KX <= 21, and for KX = 7 / 9 only when a launch carries a single z-slice of taps
+// (both instantiations exist for those two widths); scalar FFMA otherwise.
+#ifndef NDC_FFMA2
+#define NDC_FFMA2 1
+#endif
+enum PackMode : int { kPackNever = 0, kPackAlways = 1, kPackSingleSlice = 2 };
+template <int KX>
+__host__ __device__ constexpr int pack_mode() {
+  return !NDC_FFMA2 ? kPackNever : (KX >= 11 && KX <= 21) ? kPackAlways : (KX == 7 || KX == 9) ? kPackSingleSlice : kPackNever;
+}
+
+template <bool PK>
+struct RowAcc {  // scalar: one partial sum per output column
+  float v[kRX];
+};
+template <>
+struct RowAcc<true> {  // packed: even-tap pairs a, odd-tap pairs b (columns 1..14), b0, b15
+  float2 a[kRX / 2];
+  float2 b[kRX / 2 - 1];
+  float b0, b15;
+};
+
+__device__ __forceinline__ void row_zero(RowAcc<false>& r) {
+#pragma unroll
+  for (int c = 0; c < kRX; ++c) r.v[c] = 0.f;
+}
+__device__ __forceinline__ void row_zero(RowAcc<true>& r) {
+#pragma unroll
+  for (int c = 0; c < kRX / 2; ++c) r.a[c] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < kRX / 2 - 1; ++c) r.b[c] = make_float2(0.f, 0.f);
+  r.b0 = r.b15 = 0.f;
+}
+__device__ __forceinline__ void row_value(const RowAcc<false>& r, float (&o)[kRX]) {
+#pragma unroll
+  for (int c = 0; c < kRX; ++c) o[c] = r.v[c];
+}
+__device__ __forceinline__ void row_value(const RowAcc<true>& r, float (&o)[kRX]) {
+#pragma unroll
+  for (int c = 0; c < kRX / 2; ++c) {
+    o[2 * c] = r.a[c].x;
+    o[2 * c + 1] = r.a[c].y;
+  }
+  o[0] += r.b0;
+#pragma unroll
+  for (int c = 0; c < kRX / 2 - 1; ++c) {
+    o[2 * c + 1] += r.b[c].x;
+    o[2 * c + 2] += r.b[c].y;
+  }
+  o[kRX - 1] += r.b15;
+}
+
 // NR of the thread's RY row windows against every tap row of one staged plane.
-template <int KX, int SH, int RY, int NR, bool STRIDED>
-__device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const float* base,
+template <int KX, int SH, int RY, int NR, bool STRIDED, bool PK>
+__device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const float* base,
                                                 const float* trow, int KY, int ky0, int kys,
                                                 int pitch_s) {
   constexpr int NQ = window_quads(KX, SH);
@@ -356,11 +424,32 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
         win[4 * q + 2] = v.z;
         win[4 * q + 3] = v.w;
       }
+      if constexpr (PK) {
+      static_assert(SH % 2 == 0, "window pairs must start at even registers");
+      static_assert(kRX == 16, "column pairing assumes 16-column strips");
+#pragma unroll
+      for (int kx = 0; kx < KX; ++kx) {
+        const float t = w[kx];
+        const float* wv = win + SH + kx;
+        if (kx % 2 == 0) {
+#pragma unroll
+          for (int c = 0; c < kRX / 2; ++c)
+            acc[j].a[c] = __ffma2_rn(make_float2(t, t), make_float2(wv[2 * c], wv[2 * c + 1]), acc[j].a[c]);
+        } else {
+          acc[j].b0 = fmaf(t, wv[0], acc[j].b0);
+#pragma unroll
+          for (int c = 0; c < kRX / 2 - 1; ++c)
+            acc[j].b[c] = __ffma2_rn(make_float2(t, t), make_float2(wv[2 * c + 1], wv[2 * c + 2]), acc[j].b[c]);
+          acc[j].b15 = fmaf(t, wv[kRX - 1], acc[j].b15);
+        }
+      }
+      } else {
 #pragma unroll
       for (int kx = 0; kx < KX; ++kx) {
         const float t = w[kx];
 #pragma unroll
-        for (int c = 0; c < kRX; ++c) acc[j][c] = fmaf(t, win[SH + c + kx], acc[j][c]);
+        for (int c = 0; c < kRX; ++c) acc[j].v[c] = fmaf(t, win[SH + c + kx], acc[j].v[c]);
+      }
       }
     }
   }
@@ -378,6 +467,9 @@ __device__ __forceinline__ void accumulate_rows(float (&acc)[RY][kRX], const flo
 #ifndef NDC_SMALL_KX
 #define NDC_SMALL_KX kSmallMaxKX
 #endif
+#ifndef NDC_PREFETCH_KX
+#define NDC_PREFETCH_KX kPrefetchMaxKX  // cp.async aux_in prefetch (single-plane PSFs) up to this KX
+#endif
 // Small kernels (KX <= NDC_SMALL_KX) are HBM-bound: more resident CTAs per SM keep more
 // tile loads in flight.
 template <int KX>
@@ -392,7 +484,7 @@ constexpr int min_blocks_for() { return KX <= NDC_SMALL_KX ? NDC_SMALL_MIN_BLOCK
 // time with idle warps (config 3 forward: 47 -> 52 TFLOP/s).  Two instantiations keep the
 // interior kernel's code free of the edge logic (sharing it moved the taps off the
 // uniform datapath: -12 % on config 4).
-template <int KX, int SH, int RY, bool EDGE>
+template <int KX, int SH, int RY, bool EDGE, bool PK>
 __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     correlate_kernel(const __grid_constant__ CUtensorMap map, const CorrGeom g, const CorrArgs a,
                      const __grid_constant__ TapBlock taps) {
@@ -496,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   // Small PSFs: prefetch the epilogue's aux_in strip (Y or x) into shared memory now,
   // so it arrives during the FFMA loop instead of stalling the epilogue.
   const float* wpre = nullptr;
-  if (KX <= NDC_STAGED_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
+  if (KX <= NDC_PREFETCH_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
       !(EDGE && compact)) {
     float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
                  warp * (RY * 32 * kRX);
@@ -519,11 +611,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     wpre = pre;
   }
 
-  float acc[RY][kRX];
+  RowAcc<PK> acc2[RY];
 #pragma unroll
-  for (int j = 0; j < RY; ++j)
-#pragma unroll
-    for (int c = 0; c < kRX; ++c) acc[j][c] = 0.f;
+  for (int j = 0; j < RY; ++j) row_zero(acc2[j]);
 
   // Rows blocks / column strips entirely outside the output (the last tiles of an
   // extent that is not a tile multiple) skip their FFMAs; the test is warp-uniform.
@@ -541,9 +631,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
              : reinterpret_cast<const float*>(smem_raw + s * sbytes) + (wy * (32 * RY) + lane) * g.pitch_s + wx * kRX;
     const float* trow = taps.t + (kzA + i - g.kz0) * g.KY * tap_pitch(KX);
     if (nrun == RY)
-      accumulate_rows<KX, SH, RY, RY, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
+      accumulate_rows<KX, SH, RY, RY, EDGE, PK>(acc2, base, trow, g.KY, phase, nph, g.pitch_s);
     else if (RY > 1 && nrun == 1)
-      accumulate_rows<KX, SH, RY, 1, EDGE>(acc, base, trow, g.KY, phase, nph, g.pitch_s);
+      accumulate_rows<KX, SH, RY, 1, EDGE, PK>(acc2, base, trow, g.KY, phase, nph, g.pitch_s);
     if (i + g.stages < n) {
       __syncthreads();  // every warp is done with stage s before it is refilled
       if (tid == 0) {
@@ -554,6 +644,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
       }
     }
   }
+
+  float acc[RY][kRX];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) row_value(acc2[j], acc[j]);
 
   if (EDGE && P < 8) {
     // fold the tap-row phases of each (strip, block) pair into its phase-0 warp, in
@@ -597,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
     epilogue_tile<M, RY, false>(g, a, b, oz, tx0 + lane_col, ty0 + lane_row - lane, lane, acc, wst, nullptr, \
                                 p0, p1);                                                                \
   else                                                                                                \
-    epilogue_tile<M, RY, (KX <= NDC_STAGED_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, \
+    epilogue_tile<M, RY, (KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, \
                                                wst, wpre, p0, p1)
   switch (phase != 0 ? -2 : g.final_chunk ? g.mode : -1) {  // -2: folded into a phase-0 warp
     case kEpiStore: NDC_EPI(kEpiStore); break;
@@ -633,14 +727,21 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
                       const TapBlock& taps, int batch, int nz_out, cudaStream_t s, cudaStream_t s_edge) {
   // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
   const size_t smem = correlate_smem_bytes(g) +
-                      ((KX <= NDC_STAGED_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
+                      ((KX <= NDC_PREFETCH_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
+  // packed FFMA2 tap loop (see pack_mode): edge tiles only where it is always on
+  constexpr int kPM = pack_mode<KX>();
+  constexpr bool kPkFull = kPM != kPackNever, kPkEdge = kPM == kPackAlways;
+  const bool pk = kPM == kPackAlways || (kPM == kPackSingleSlice && g.kz1 - g.kz0 == 1);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, false>,
+    cudaError_t e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, false, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess && kPkFull)
+      e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, false, kPkFull>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               200 * 1024);
+      e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, true, kPkEdge>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -648,11 +749,16 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
   const int n_full = g.full_tx * g.full_ty;
   const int n_edge = g.tiles_x * g.tiles_y - n_full;
   if (n_full > 0) {
-    correlate_kernel<KX, SH, RY, false><<<dim3(n_full, nz_out, batch), kThreads, smem, s>>>(map, g, a, taps);
+    const dim3 grid(n_full, nz_out, batch);
+    if (pk)
+      correlate_kernel<KX, SH, RY, false, kPkFull><<<grid, kThreads, smem, s>>>(map, g, a, taps);
+    else
+      correlate_kernel<KX, SH, RY, false, false><<<grid, kThreads, smem, s>>>(map, g, a, taps);
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
   }
   if (n_edge > 0)
-    correlate_kernel<KX, SH, RY, true><<<dim3(n_edge, nz_out, batch), kThreads, smem, s_edge>>>(map, g, a, taps);
+    correlate_kernel<KX, SH, RY, true, kPkEdge><<<dim3(n_edge, nz_out, batch), kThreads, smem, s_edge>>>(map, g, a,
+                                                                                                      taps);
   return cudaGetLastError();
 }
 

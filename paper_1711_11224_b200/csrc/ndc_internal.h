@@ -36,6 +36,13 @@ constexpr int kMaxStages = 3;
 // of the epilogue's aux_in strip); up to kSmallMaxKX also 64-row tiles at 4 CTAs / SM.
 constexpr int kStagedMaxKX = 9;
 constexpr int kSmallMaxKX = 5;
+// Single-plane PSFs up to kPrefetchMaxKX prefetch the epilogue's aux_in strip with
+// cp.async at kernel start (its global-load latency otherwise stalls every warp at the
+// end of a tile).
+#ifndef NDC_PREFETCH_MAXKX
+#define NDC_PREFETCH_MAXKX 9
+#endif
+constexpr int kPrefetchMaxKX = NDC_PREFETCH_MAXKX;
 
 // Epilogue selector (uniform per launch).
 enum EpiMode : int {

@@ -625,7 +625,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
         g.kz0 = ch.kz0;
         g.kz1 = ch.kz1;
         g.stages = std::min(stages_, g.kz1 - g.kz0);
-        g.aux_prefetch = (KZ_ == 1 && KX_ <= kStagedMaxKX) ? 1 : 0;
+        g.aux_prefetch = (KZ_ == 1 && (KX_ <= kStagedMaxKX || KX_ <= kPrefetchMaxKX)) ? 1 : 0;
         g.accum = c > 0;
         g.final_chunk = (c + 1 == chunks.size());
         // x-shaped operands are addressed from their interior origin

@@ -218,3 +218,28 @@ def test_edge_tiles_few_rows(nd, oracle_c, xs, hs):
     assert got.iterations_run == want.iterations_run
     assert rel_l2(got.estimate, want.estimate) <= 1e-4
     np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
+
+
+@pytest.mark.parametrize("xs,hs", [((130, 150), (7, 7)), ((150, 130), (9, 9)), ((140, 140), (11, 11)),
+                                   ((129, 200), (13, 13)), ((200, 129), (17, 17)), ((150, 160), (21, 21)),
+                                   ((5, 70, 90), (3, 9, 9)), ((5, 70, 90), (3, 11, 19)), ((4, 64, 64), (3, 7, 7))])
+def test_packed_ffma2_widths(nd, oracle_c, xs, hs):
+    """PSF widths whose tap loop runs packed FFMA2 (11..21 always, 7 / 9 for single-slice
+    launches) and their scalar 3-D counterparts: every element of forward and adjoint
+    (full and edge tiles) and a short PG run against the oracle."""
+    rng = np.random.default_rng(sum(xs) * 7 + sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    y_ref = oracle_c.conv_full(x, h)
+    assert rel_l2(nd.conv_full(x, h), y_ref) <= TOL_CONV
+    assert np.max(np.abs(nd.conv_full(x, h) - y_ref)) <= 1e-5 * np.max(np.abs(y_ref))
+    r = rng.uniform(-1, 1, y_ref.shape)
+    a_ref = oracle_c.adjoint_apply(r, h, xs)
+    assert np.max(np.abs(nd.adjoint_apply(r, h, xs) - a_ref)) <= 1e-5 * np.max(np.abs(a_ref))
+    yo = y_ref + rng.uniform(0, 1e-3, y_ref.shape)
+    cfg = nd.DeconvConfig(max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    got = nd.deconv_pg(yo, h, xs, cfg)
+    want = oracle_c.deconv_pg(yo, h, xs, max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    assert got.iterations_run == want.iterations_run
+    assert rel_l2(got.estimate, want.estimate) <= 1e-4

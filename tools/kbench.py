@@ -17,9 +17,11 @@ a = ap.parse_args()
 SHAPES = {"c2": (16, (2048, 2048)), "c3": (1, (128, 256, 256)), "c4": (1, (512, 1024, 1024)),
           "c4s": (1, (64, 1024, 1024)), "c5s": (1, (16, 2048, 2048)), "c1": (1, (256, 256)),
           "c2k1": (16, (2048, 2048)), "c2k3": (16, (2048, 2048)), "c2k5": (16, (2048, 2048)),
-          "c2k9": (16, (2048, 2048))}
+          "c2k9": (16, (2048, 2048)), "c2k11": (16, (2048, 2048)), "c2k13": (16, (2048, 2048)),
+          "c2k15": (16, (2048, 2048)), "c2k17": (16, (2048, 2048)), "c2k21": (16, (2048, 2048)),
+          "c2k25": (16, (2048, 2048)), "c2k33": (16, (2048, 2048))}
 for name in a.configs:
-    B, xs = SHAPES[name]
+    B, xs = SHAPES[name] if name in SHAPES else (16, (2048, 2048))  # c2k<N>: N x N Gaussian
     if name == "c2k1":
         h = np.ones((1, 1))
     elif name.startswith("c2k"):
