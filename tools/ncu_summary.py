@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches_r01.csv profiles/r01_launches.md
     python tools/ncu_summary.py full gpurun_out/prof_r01.ncu-rep profiles/r01_correlate_full.md
+    python tools/ncu_summary.py full gpurun_out/prof_r01_raw.csv profiles/r01_correlate_full.md
 
 `launches`: per-kernel launch counts, total / mean device time and share (the ncu
 per-launch times are cold-cache and serialised -- compare shares, not absolutes).
@@ -69,7 +70,12 @@ METRICS = [
 
 
 def full(path: str, out: str):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .ncu-rep, or its `--page raw --csv` export (exported on the GPU box when the
+    # report itself is too large to bring back)
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rdr = list(csv.reader(io.StringIO(raw)))
     if len(rdr) < 3:
         raise SystemExit("no data in " + path)
