@@ -103,6 +103,9 @@ class Plan {
   bool kernel_all_zero() const { return kernel_all_zero_; }
   double estimate_collect();
   double estimate_step_f64(size_t power_iters);  // small problems (reference-exact)
+  // separable PSFs: the power iteration as a product of 1-D iterations (host, f64);
+  // false if h is not rank-1
+  bool estimate_step_separable(size_t power_iters, double* step);
 
   // --- projected gradient (solvers.hpp:155-238) ---
   void pg_begin(const ndc_deconv_config& cfg);
