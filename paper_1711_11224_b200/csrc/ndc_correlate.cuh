@@ -95,8 +95,12 @@ __host__ __device__ constexpr int stage_bytes_aligned(int rows, int pitch_s) {
 // stages, so no warp ever waits for another around the epilogue.
 constexpr int kStagingBytes = (kThreads / 32) * 32 * kRX * 4;
 
-// Dynamic shared memory: stages, staging, then the stage mbarriers.
-__host__ __device__ constexpr int barrier_offset(int stages, int sbytes) { return stages * sbytes + kStagingBytes; }
+// Dynamic shared memory: stages, staging (staged-epilogue kernels only), then the stage
+// mbarriers.  The direct-epilogue (large-PSF) kernels carry no staging buffer: 16 KB less
+// per CTA lets a third CTA share the SM when registers allow (config 2: 3 x 63 KB).
+__host__ __device__ constexpr int barrier_offset(int stages, int sbytes, bool staging) {
+  return stages * sbytes + (staging ? kStagingBytes : 0);
+}
 
 // p0 combines with max for the KKT-style epilogues, with + otherwise.
 __device__ __forceinline__ bool p0_is_max(int mode) { return mode == kEpiPG || mode == kEpiKKT; }
@@ -467,6 +471,9 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
 #ifndef NDC_SMALL_KX
 #define NDC_SMALL_KX kSmallMaxKX
 #endif
+#ifndef NDC_NOSTAGING_DIRECT
+#define NDC_NOSTAGING_DIRECT 1  // direct-epilogue kernels allocate no staging buffer
+#endif
 #ifndef NDC_PREFETCH_KX
 #define NDC_PREFETCH_KX kPrefetchMaxKX  // cp.async aux_in prefetch (single-plane PSFs) up to this KX
 #endif
@@ -474,6 +481,19 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
 // tile loads in flight.
 template <int KX>
 constexpr int min_blocks_for() { return KX <= NDC_SMALL_KX ? NDC_SMALL_MIN_BLOCKS : NDC_MIN_BLOCKS; }
+#ifndef NDC_DIRECT_MIN_BLOCKS
+#define NDC_DIRECT_MIN_BLOCKS 3
+#endif
+// Residency target per instantiation: the scalar direct-epilogue 128-row (RY = 2) kernels
+// of large PSFs (config 2) ask for 3 CTAs / SM -- 80 registers, no spills, and their shared
+// memory carries no staging buffer (3 x 63 KB).  Measured (tools/kbench.py): config 2
+// +0.4..0.8 %, 2048^2 x 16 with 25 x 25 taps +1..5 %; the 64-row 3-D kernels (config 5)
+// lose 0.8 % at 3 and keep 2.
+template <int KX, int RY, bool EDGE, bool PK>
+constexpr int min_blocks_of() {
+  return (RY == 2 && !PK && !EDGE && KX > NDC_STAGED_KX && KX > NDC_PREFETCH_KX) ? NDC_DIRECT_MIN_BLOCKS
+                                                                                 : min_blocks_for<KX>();
+}
 
 // EDGE = false: the full tiles (tx < full_tx, ty < full_ty).  EDGE = true: the partial
 // tiles of extents that are not tile multiples (last tile column / row).  An edge tile has
@@ -485,7 +505,7 @@ constexpr int min_blocks_for() { return KX <= NDC_SMALL_KX ? NDC_SMALL_MIN_BLOCK
 // interior kernel's code free of the edge logic (sharing it moved the taps off the
 // uniform datapath: -12 % on config 4).
 template <int KX, int SH, int RY, bool EDGE, bool PK>
-__global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
+__global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     correlate_kernel(const __grid_constant__ CUtensorMap map, const CorrGeom g, const CorrArgs a,
                      const __grid_constant__ TapBlock taps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -566,7 +586,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   const int n = kzB - kzA;
 
   const int sbytes = stage_bytes_aligned(g.rows, g.pitch_s);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + barrier_offset(g.stages, sbytes));
+  constexpr bool kStaging = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX || !NDC_NOSTAGING_DIRECT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + barrier_offset(g.stages, sbytes, kStaging));
   const uint32_t tx_bytes = static_cast<uint32_t>(g.rows * g.pitch_s * 4);
 
   if (tid == 0) {
@@ -590,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_for<KX>())
   const float* wpre = nullptr;
   if (KX <= NDC_PREFETCH_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
       !(EDGE && compact)) {
-    float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes) + 128) +
+    float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes, kStaging) + 128) +
                  warp * (RY * 32 * kRX);
     const int ox0 = tx0 + wx * kRX;
     const long long obase = static_cast<long long>(b) * g.out_image +
@@ -726,7 +747,8 @@ template <int KX, int SH, int RY>
 cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs& a,
                       const TapBlock& taps, int batch, int nz_out, cudaStream_t s, cudaStream_t s_edge) {
   // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
-  const size_t smem = correlate_smem_bytes(g) +
+  constexpr bool kStaging = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX || !NDC_NOSTAGING_DIRECT;
+  const size_t smem = correlate_smem_bytes(g, kStaging) +
                       ((KX <= NDC_PREFETCH_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
   // packed FFMA2 tap loop (see pack_mode): edge tiles only where it is always on
   constexpr int kPM = pack_mode<KX>();
@@ -742,6 +764,11 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, true, kPkEdge>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // 3-CTA kernels (min_blocks_of): full shared-memory carveout so the third CTA fits
+    // (the 64-row 3-D kernels keep the default: config 5 measured -1 % with it)
+    if (e == cudaSuccess && min_blocks_of<KX, RY, false, false>() >= 3)
+      e = cudaFuncSetAttribute(correlate_kernel<KX, SH, RY, false, false>,
+                               cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = true;
   }

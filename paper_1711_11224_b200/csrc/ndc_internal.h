@@ -121,7 +121,7 @@ NDC_DECL_CORR(0, 2)
 NDC_DECL_CORR(2, 1)
 NDC_DECL_CORR(2, 2)
 #undef NDC_DECL_CORR
-size_t correlate_smem_bytes(const CorrGeom& g);
+size_t correlate_smem_bytes(const CorrGeom& g, bool staging);
 int shared_pitch_for(int kx, int sh);
 
 // Small kernels.

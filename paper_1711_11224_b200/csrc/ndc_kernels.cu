@@ -265,9 +265,8 @@ int shared_pitch_for(int kx, int sh) {
   return p;
 }
 
-size_t correlate_smem_bytes(const CorrGeom& g) {
-  // stage 0 doubles as the epilogue's per-warp staging buffers
-  return static_cast<size_t>(corr::barrier_offset(g.stages, corr::stage_bytes_aligned(g.rows, g.pitch_s))) +
+size_t correlate_smem_bytes(const CorrGeom& g, bool staging) {
+  return static_cast<size_t>(corr::barrier_offset(g.stages, corr::stage_bytes_aligned(g.rows, g.pitch_s), staging)) +
          static_cast<size_t>(kMaxStages) * 8;
 }
 
