@@ -116,7 +116,11 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     const long long pitch2 = std::max(shared_pitch_for(kcx_, 0), shared_pitch_for(kcx_, 2));
     const long long stage2 = static_cast<long long>(2 * kTileY + KY_ - 1) * pitch2 * 4;
     const bool fits = 2 * kTileY + KY_ - 1 <= kMaxRows;
-    ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= 90 * 1024)) ? 2 : 1;
+    // two CTAs per SM: staged-epilogue kernels (KX <= kStagedMaxKX) also carry a 16 KB
+    // staging buffer; the direct-epilogue ones do not (config 3 runs RY = 2 since then:
+    // adjoint +2 %, forward unchanged)
+    const long long budget = (kcx_ <= kStagedMaxKX ? 90 : 110) * 1024LL;
+    ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= budget)) ? 2 : 1;
     // small PSFs are HBM-bound: 64-row tiles at 4 CTAs / SM keep more loads in flight
     if (KX_ <= kSmallMaxKX) ry_ = 1;
   }
