@@ -400,6 +400,13 @@ __device__ __forceinline__ void row_value(const RowAcc<true>& r, float (&o)[kRX]
   o[kRX - 1] += r.b15;
 }
 
+// Tap-row loop unroll (a tuning knob; measured: 2 or 3 costs 10-30 % on configs 2-4 --
+// the unrolled body no longer keeps the taps on the uniform datapath).
+#ifndef NDC_KY_UNROLL
+#define NDC_KY_UNROLL 1
+#endif
+constexpr int kKyUnroll = NDC_KY_UNROLL;
+
 // NR of the thread's RY row windows against every tap row of one staged plane.
 template <int KX, int SH, int RY, int NR, bool STRIDED, bool PK>
 __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const float* base,
@@ -410,6 +417,7 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
   // Tap rows 0..KY-1 (STRIDED, edge tiles only: ky0, ky0 + kys, ...).  In the interior
   // kernel the induction variable is uniform, which keeps the tap loads on the uniform
   // datapath (LDCU -> FFMA R, R, UR).
+#pragma unroll kKyUnroll
   for (int ky = STRIDED ? ky0 : 0; ky < KY; ky += STRIDED ? kys : 1) {
     const float* w = trow + ky * KXP;
 #if defined(NDC_J_NOUNROLL)
