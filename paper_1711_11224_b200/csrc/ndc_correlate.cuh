@@ -67,6 +67,15 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// L2 prefetch of the two 32-byte sectors of a 64-byte row segment (no register result).
+#ifndef NDC_L2_PREFETCH
+#define NDC_L2_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const float* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 8));
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -611,6 +620,27 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
       mbar_expect_tx(&bars[i], tx_bytes);
       tma_load_3d(smem_raw + i * sbytes, &map, &bars[i], tx0 + g.off_x, ty0 + g.off_y,
                   b * g.in_ez + iz);
+    }
+  }
+
+  // Kernels without the shared-memory aux prefetch below (large PSFs, 3-D volumes): ask
+  // L2 for the rows the epilogue will read (aux_in and the earlier chunks' partial sums)
+  // now, so they are on chip when the tap loop ends instead of costing a DRAM round trip.
+  if constexpr (NDC_L2_PREFETCH && !EDGE) {
+    const bool aux = g.final_chunk && mode_reads_aux_rt(g.mode) && !(KX <= NDC_PREFETCH_KX && g.aux_prefetch);
+    const int ox0 = tx0 + wx * kRX;
+    if ((aux || g.accum) && ox0 < g.out_ex) {
+      const long long obase = static_cast<long long>(b) * g.out_image +
+                              static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        const int row = ty0 + wy * (32 * RY) + 32 * j + lane;
+        if (row < g.out_ey) {
+          const long long o = obase + static_cast<long long>(row) * g.out_pitch;
+          if (aux) prefetch_l2(a.aux_in + o);
+          if (g.accum) prefetch_l2(a.accum_in + o);
+        }
+      }
     }
   }
 

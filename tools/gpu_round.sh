@@ -15,7 +15,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 $SHORT > gpurun_out/short_$TAG.json 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
       --log-file gpurun_out/launches_$TAG.csv $SHORT > gpurun_out/ncu_launch_$TAG.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:correlate -s 100 -c 2 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:correlate -s 10 -c 2 \
       -o gpurun_out/prof_$TAG $SHORT > gpurun_out/ncu_full_$TAG.log 2>&1
   echo "ncu rc=$?"
 fi
