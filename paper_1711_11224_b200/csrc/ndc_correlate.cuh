@@ -69,7 +69,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Output-plane-fastest CTA order for 3-D launches (see correlate_kernel).  Measured
 // (profiles/r01m_kbench_z_fast.txt): config 4 forward DRAM reads 35.9 -> 5.1 GB per pass
-// (the KZ = 21 input planes of a tile stay in L2), config 5 forward +2.4 %, others equal.
+// (the KZ = 21 input planes of a tile stay in L2); step times equal within 0.3 %.
 #ifndef NDC_Z_FAST
 #define NDC_Z_FAST 1
 #endif
