@@ -67,6 +67,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Edge-tile tap-row split by a uniform loop with per-warp skips (see accumulate_rows).
+#ifndef NDC_EDGE_UNIFORM
+#define NDC_EDGE_UNIFORM 0
+#endif
+
 // Output-plane-fastest CTA order for 3-D launches (see correlate_kernel).  Measured
 // (profiles/r01m_kbench_z_fast.txt): config 4 forward DRAM reads 35.9 -> 5.1 GB per pass
 // (the KZ = 21 input planes of a tile stay in L2); step times equal within 0.3 %.
@@ -434,7 +439,10 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
   // kernel the induction variable is uniform, which keeps the tap loads on the uniform
   // datapath (LDCU -> FFMA R, R, UR).
 #pragma unroll kKyUnroll
-  for (int ky = STRIDED ? ky0 : 0; ky < KY; ky += STRIDED ? kys : 1) {
+  for (int ky = (STRIDED && !NDC_EDGE_UNIFORM) ? ky0 : 0; ky < KY; ky += (STRIDED && !NDC_EDGE_UNIFORM) ? kys : 1) {
+    // edge tiles (NDC_EDGE_UNIFORM): walk every tap row with a uniform induction variable
+    // (taps stay on the uniform datapath) and skip the rows of the other phases
+    if (STRIDED && NDC_EDGE_UNIFORM && ky % kys != ky0) continue;
     const float* w = trow + ky * KXP;
 #if defined(NDC_J_NOUNROLL)
 #pragma unroll 1
