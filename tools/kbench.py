@@ -22,6 +22,8 @@ SHAPES = {"c2": (16, (2048, 2048)), "c3": (1, (128, 256, 256)), "c4": (1, (512, 
           "c2k25": (16, (2048, 2048)), "c2k33": (16, (2048, 2048))}
 for name in a.configs:
     B, xs = SHAPES[name] if name in SHAPES else (16, (2048, 2048))  # c2k<N>: N x N Gaussian
+    if name.startswith("c2b"):  # c2b<N>: config 2 with a batch of N images (wave-tail sizing)
+        B, name = int(name[3:]), "c2"
     if name == "c2k1":
         h = np.ones((1, 1))
     elif name.startswith("c2k"):
