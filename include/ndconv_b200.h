@@ -213,6 +213,10 @@ ndc_status ndc_plan_pg_begin(ndc_plan* plan, const ndc_deconv_config* cfg);
 ndc_status ndc_plan_pg_iterate(ndc_plan* plan, size_t n, size_t* images_active);
 ndc_status ndc_plan_pg_end(ndc_plan* plan);
 ndc_status ndc_plan_pg_run(ndc_plan* plan, const ndc_deconv_config* cfg);
+/* Richardson-Lucy (deconv_rl, solvers.hpp:245-305) on the resident observation, which it
+ * leaves unchanged (the clamped copy lives in plan scratch for the run); per-image
+ * results through ndc_plan_get_report / ndc_plan_get_estimate_*. */
+ndc_status ndc_plan_rl_run(ndc_plan* plan, const ndc_rl_config* cfg);
 /* Per-image results after pg_end; traces need trace_cap entries per image. */
 ndc_status ndc_plan_get_report(ndc_plan* plan, size_t image, ndc_deconv_report* report,
                                double* obj_trace, double* kkt_trace, size_t trace_cap);

@@ -6,6 +6,10 @@ Two interchangeable back ends with identical signatures:
   reference algorithm (``oracle/ndconv_oracle.c``);
 * ``"ref"`` -- ``oracle/_ref/libndconv_ref.so``, the unmodified reference headers
   (``/root/reference/proj/include``) compiled behind a C shim (``oracle/ref_shim.cpp``).
+* ``"fast"`` -- ``oracle/_build/libndconv_fast.so``, the same algorithm with threaded,
+  vectorised float64 convolutions (``oracle/ndconv_fast.c``) for config-scale parity:
+  conv_full / adjoint_apply / estimate_step / deconv_pg only, pinned to the "c" oracle
+  to ~1e-12 by tests/test_oracle.py.
 
 Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs may import
 this module.  The product package never does.
@@ -22,8 +26,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "c": os.path.join(HERE, "_build", "libndconv_oracle.so"),
     "ref": os.path.join(HERE, "_ref", "libndconv_ref.so"),
+    "fast": os.path.join(HERE, "_build", "libndconv_fast.so"),
 }
-PREFIX = {"c": "oc_", "ref": "ref_"}
+PREFIX = {"c": "oc_", "ref": "ref_", "fast": "of_"}
 
 RC_NAMES = {1: "Error", 2: "ShapeError", 3: "NumericError", 4: "BoundsError", 5: "FormatError", 9: "Other"}
 STOP_NAMES = {0: "converged", 1: "max_iters", 2: "stalled"}
@@ -171,11 +176,15 @@ class Oracle:
         kt = np.empty(max_iters + 1, np.float64)
         tl, it, bt = C.c_size_t(), C.c_size_t(), C.c_size_t()
         sr = C.c_int()
+        st = C.c_double()
+        more = (C.byref(st),) if self.kind == "fast" else ()
         self._call("deconv_pg", C.c_int(y.ndim), _ext(y.shape), _ptr(y), _ext(h.shape), _ptr(h),
                    _ext(x_shape), C.byref(cfg), _ptr(x), _ptr(ot), _ptr(kt), C.byref(tl), C.byref(it),
-                   C.byref(sr), C.byref(bt))
+                   C.byref(sr), C.byref(bt), *more)
         n = tl.value
         extra = {} if self.kind == "ref" else {"backtracks": bt.value}
+        if self.kind == "fast":
+            extra["step0"] = st.value
         return Report(x, ot[:n].copy(), kt[:n].copy(), it.value, STOP_NAMES[sr.value], extra)
 
     def deconv_rl(self, y, h, x_shape, max_iters=500, tol_rel_change=0.0) -> Report:

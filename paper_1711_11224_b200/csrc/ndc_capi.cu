@@ -417,6 +417,9 @@ ndc_status ndc_plan_pg_run(ndc_plan* plan, const ndc_deconv_config* cfg) {
   NDC_PLAN(const ndc_deconv_config c = cfg ? *cfg : default_cfg(); plan->p->pg_begin(c);
            plan->p->pg_iterate(c.max_iters); plan->p->pg_end());
 }
+ndc_status ndc_plan_rl_run(ndc_plan* plan, const ndc_rl_config* cfg) {
+  NDC_PLAN(ndc_rl_config c; ndc_rl_config_default(&c); if (cfg) c = *cfg; plan->p->rl_run(c));
+}
 ndc_status ndc_plan_get_report(ndc_plan* plan, size_t image, ndc_deconv_report* report,
                                double* obj_trace, double* kkt_trace, size_t trace_cap) {
   NDC_PLAN(need(report, "report"); plan->p->get_report(image, report, obj_trace, kkt_trace, trace_cap));

@@ -235,16 +235,17 @@ Plan::~Plan() {
 // raised, so destroying and re-creating plans (every one-shot C-ABI call) reuses HBM
 // instead of paying cudaMalloc / cudaFree each time.
 void* Plan::dmalloc(size_t bytes) {
-  static bool pool_set[64] = {};
-  if (device_ < 64 && !pool_set[device_]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-    pool_set[device_] = true;
-  }
+  // once per device; plans of in-process slab ranks are created from concurrent threads
+  static std::once_flag pool_set[64];
+  if (device_ < 64)
+    std::call_once(pool_set[device_], [this] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+    });
   void* p = nullptr;
   check_cuda(cudaMallocAsync(&p, bytes, stream_), "cudaMallocAsync");
   return p;
@@ -1029,8 +1030,6 @@ double Plan::estimate_step(size_t power_iters) {
 void Plan::estimate_launch(size_t power_iters) {
   drain_halos();
   if (power_iters == 0) fail(NDC_ERR_CONFIG, "estimate_step: power_iters must be positive");
-  if (power_iters > static_cast<size_t>(kMaxPowerIters))
-    fail(NDC_ERR_UNSUPPORTED, "estimate_step: power_iters too large");
   if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "estimate_step: degenerate all-zero kernel");
   const double n = static_cast<double>(mz_) * my_ * mx_;
   estimate_pending_ = 0;
@@ -1068,9 +1067,10 @@ void Plan::estimate_launch(size_t power_iters) {
       correlate(kFwd, g_, rt_, kEpiStore, nullptr, nullptr, dscale_, nullptr, nullptr, false);
       halo_y(rt_);
       correlate(kAdj, rt_, g_, kEpiNorm, nullptr, nullptr, nullptr, nullptr, nullptr, true);
-      finalize(partials_per_image(kAdj), kFinNorm, lam + i, nullptr, dscale_, nullptr);
+      finalize(partials_per_image(kAdj), kFinNorm, lam + i % kMaxPowerIters, nullptr, dscale_, nullptr);
     }
-    check_cuda(cudaMemcpyAsync(hsc_, lam, power_iters * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+    check_cuda(cudaMemcpyAsync(hsc_, lam, lam_slots(power_iters) * 8, cudaMemcpyDeviceToHost, stream_),
+               "D2H");
   } catch (...) {
     B_ = saveB;
     maps_.clear();
@@ -1088,10 +1088,7 @@ double Plan::estimate_collect() {
   estimate_pending_ = 0;
   if (estimate_f64_) return estimate_value_;
   sync();
-  for (size_t i = 0; i < power_iters; ++i)
-    if (!(hsc_[i] > 0.0) || !std::isfinite(hsc_[i]))
-      fail(NDC_ERR_NUMERIC, "estimate_step: degenerate convolution operator");
-  const double step = 1.0 / hsc_[power_iters - 1];
+  const double step = 1.0 / collect_lambdas(power_iters);
   // restore the per-image scale to 1 for later kEpiStore users
   std::vector<float> ones(B_, 1.0f);
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
@@ -1325,22 +1322,35 @@ double Plan::estimate_step_f64(size_t power_iters) {
     // u = A v_i with v_i = w_{i-1} / lambda_{i-1} folded in as an output scale
     long long nb = 0;
     check_cuda(launch_corr_f64(v, mz_, my_, mx_, u, oz, oy, ox, dhf, KZ_, KY_, KX_, -2 * pz_, -2 * py_,
-                               -2 * px_, i ? lam + i - 1 : nullptr, nullptr, &nb, stream_),
+                               -2 * px_, i ? lam + (i - 1) % kMaxPowerIters : nullptr, nullptr, &nb, stream_),
                "corr_f64 launch");
     // w = A^T u (valid correlation), ||w||^2 per block
     check_cuda(launch_corr_f64(u, oz, oy, ox, v, mz_, my_, mx_, dh, KZ_, KY_, KX_, 0, 0, 0, nullptr, part,
                                &nb, stream_),
                "corr_f64 launch");
-    check_cuda(launch_finalize(part, nb, 1, kFinNorm, lam + i, nullptr, nullptr, nullptr, stream_),
+    check_cuda(launch_finalize(part, nb, 1, kFinNorm, lam + i % kMaxPowerIters, nullptr, nullptr, nullptr,
+                               stream_),
                "finalize launch");
     st_[2].launches += 3;
   }
-  check_cuda(cudaMemcpyAsync(hsc_, lam, power_iters * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+  check_cuda(cudaMemcpyAsync(hsc_, lam, lam_slots(power_iters) * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
   sync();
-  for (size_t i = 0; i < power_iters; ++i)
+  return 1.0 / collect_lambdas(power_iters);
+}
+
+// The device power iterations record lambda_i in a ring of kMaxPowerIters slots (any
+// power_iters is accepted, as in the reference).  A degenerate lambda (<= 0 or
+// non-finite, solvers.hpp:137-139) makes the next rescale 1/lambda infinite or NaN, so
+// every later lambda is NaN: checking the slots still held covers the whole run.
+size_t Plan::lam_slots(size_t power_iters) {
+  return std::min(power_iters, static_cast<size_t>(kMaxPowerIters));
+}
+
+double Plan::collect_lambdas(size_t power_iters) {
+  for (size_t i = 0; i < lam_slots(power_iters); ++i)
     if (!(hsc_[i] > 0.0) || !std::isfinite(hsc_[i]))
       fail(NDC_ERR_NUMERIC, "estimate_step: degenerate convolution operator");
-  return 1.0 / hsc_[power_iters - 1];
+  return hsc_[(power_iters - 1) % kMaxPowerIters];
 }
 
 // estimate_step (solvers.hpp:127-143) for a separable PSF h[z][y][x] = a[z] b[y] c[x]:
@@ -1613,6 +1623,14 @@ size_t Plan::pg_iterate(size_t n) {
       trial2_ = old_x;
       std::swap(g_, g2_);
       std::swap(r_, rt_);
+      // Images that stopped at an earlier step were skipped by both passes: the rotated
+      // x / r buffers hold stale data for them, so their last iterate and residual are
+      // copied back (pg_end's final KKT and the estimate read them).
+      for (size_t b = 0; b < B_; ++b)
+        if (!act[b]) {
+          copy_image_x(x_, old_x, b);
+          copy_image_y(r_, rt_, b);
+        }
       spec_ready_ = true;
       continue;
     }
@@ -1739,17 +1757,30 @@ void Plan::rl_run(const ndc_rl_config& c) {
     set_taps(1.0);
     std::swap(hn, h64_);
   }
+  // yc = clamp(y) goes to a y-shaped buffer of its own for the run (the reference's
+  // deconv_rl leaves y untouched: the resident observation stays the user's data)
+  float* const y_user = yobs_;
+  float* const yc = dev_alloc_f(Y_.image * static_cast<long long>(B_));
   struct Restore {
     Plan* p;
-    ~Restore() { p->set_taps(1.0); }
-  } restore{this};
+    float* y_user;
+    float* yc;
+    ~Restore() {
+      p->drain_halos();
+      p->yobs_ = y_user;
+      cudaFreeAsync(yc, p->stream_);
+      p->set_taps(1.0);
+    }
+  } restore{this, y_user, yc};
 
   img_.assign(B_, Img{});
   // yc = clamp(y), negatives counted, total = sum(yc)
   const Geo yv = Y_.geo(yb_ - ya_);
-  float* yown = yobs_ + static_cast<long long>(ya_ - rlo_) * Y_.plane;
-  check_cuda(launch_clamp_count(yown, yown, partials_, static_cast<int>(B_), yv, kElemBlocks, stream_),
+  const long long own_off = static_cast<long long>(ya_ - rlo_) * Y_.plane;
+  check_cuda(launch_clamp_count(y_user + own_off, yc + own_off, partials_, static_cast<int>(B_), yv,
+                                kElemBlocks, stream_),
              "clamp launch");
+  yobs_ = yc;  // the RL passes below read the clamped copy
   st_[2].launches++;
   finalize(kElemBlocks, kFinSumSum, dsc_ + kAUX * B_, dsc_ + kCHG * B_, nullptr, nullptr);
   check_cuda(cudaMemcpyAsync(hsc_, dsc_, kNumSlots * B_ * 8, cudaMemcpyDeviceToHost, stream_), "D2H");

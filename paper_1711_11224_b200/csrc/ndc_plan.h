@@ -102,6 +102,8 @@ class Plan {
   void estimate_launch(size_t power_iters);  // enqueue only (see ndc_plan.cu)
   bool kernel_all_zero() const { return kernel_all_zero_; }
   double estimate_collect();
+  static size_t lam_slots(size_t power_iters);
+  double collect_lambdas(size_t power_iters);
   double estimate_step_f64(size_t power_iters);  // small problems (reference-exact)
   // separable PSFs: the power iteration as a product of 1-D iterations (host, f64);
   // false if h is not rank-1

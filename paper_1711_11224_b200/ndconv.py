@@ -538,6 +538,12 @@ class Plan:
         c = (cfg or DeconvConfig()).to_c()
         _check(N.lib().ndc_plan_pg_run(self.handle, C.byref(c)))
 
+    def rl_run(self, cfg: RlConfig | None = None):
+        """deconv_rl (solvers.hpp:245-305) on the resident observation (left unchanged)."""
+        cfg = cfg or RlConfig()
+        c = N.RlConfig(int(cfg.max_iters), float(cfg.tol_rel_change))
+        _check(N.lib().ndc_plan_rl_run(self.handle, C.byref(c)))
+
     def estimate(self, dtype=np.float64) -> np.ndarray:
         x = np.empty((self.batch,) + self.owned_x_shape(), dtype)
         if dtype == np.float32:

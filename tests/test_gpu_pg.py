@@ -269,3 +269,105 @@ def test_speculative_adjoint_is_bit_identical(tmp_path):
         outs.append(np.load(out))
     assert outs[0].shape == outs[1].shape
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+# Staggered stops: the oracle stops these c1-like images by tolerance at
+# iterations 33, 37 and 39 (drop / tol margins >= 1.6 % at and before the stop, so the
+# float32 objective cannot move a stop by one), and the all-negative image converges at
+# once.  The images keep running for several steps after the first ones stop, with the
+# speculative next-step adjoint kept on every step where all active images accept.
+_STAGGER = (
+    "import sys, numpy as np\n"
+    "sys.path.insert(0, %r)\n"
+    "from paper_1711_11224_b200 import synth\n"
+    "x, y, h = synth.make('c1', batch=4, shape=(40, 36), n_objects=8)\n"
+    "y = np.stack([y[0], y[2], y[3], -np.abs(y[1]) - 0.1])\n")
+
+
+def _stagger_inputs():
+    ns = {}
+    exec(_STAGGER % ROOT, ns)
+    return ns["y"], ns["h"], (40, 36)
+
+
+def test_batch_staggered_stops_vs_oracle(nd, oracle_c):
+    y, h, xs = _stagger_inputs()
+    cfg = nd.DeconvConfig(max_iters=80, tol_rel_objective=2e-3)
+    reps = nd.deconv_pg_batch(y, h, xs, cfg)
+    its = []
+    for b in range(4):
+        ref = oracle_c.deconv_pg(y[b], h, xs, max_iters=80, tol_rel_objective=2e-3)
+        assert reps[b].stop_reason == ref.stop_reason == "converged", b
+        assert reps[b].iterations_run == ref.iterations_run, (b, reps[b].iterations_run, ref.iterations_run)
+        assert rel_l2(reps[b].estimate, ref.estimate) <= TOL_ITER or np.max(np.abs(reps[b].estimate)) == 0.0, b
+        assert _trace_close(reps[b].objective_trace, ref.objective_trace, TOL_ITER), b
+        # the final KKT comes from the stopped image's own last iterate and residual
+        k_ref = float(ref.kkt_trace[-1])
+        assert abs(reps[b].kkt_trace[-1] - k_ref) <= 1e-3 * max(abs(float(ref.kkt_trace[0])), 1e-30), b
+        its.append(ref.iterations_run)
+    assert sorted(its)[1:] == [33, 37, 39] and its[3] == 0
+
+
+def test_batch_staggered_stops_speculation_bit_identical(tmp_path):
+    """NDC_SPECULATE=0 / 1 give the same bits on the staggered batch (the speculative
+    commit keeps the stopped images' iterates)."""
+    import subprocess
+    import sys
+    script = tmp_path / "run.py"
+    script.write_text(
+        _STAGGER % str(ROOT) +
+        "from paper_1711_11224_b200 import ndconv as nd\n"
+        "cfg = nd.DeconvConfig(max_iters=80, tol_rel_objective=2e-3)\n"
+        "res = []\n"
+        "for r in nd.deconv_pg_batch(y, h, (40, 36), cfg):\n"
+        "    res += [r.estimate.ravel(), np.asarray(r.objective_trace), np.asarray(r.kkt_trace),\n"
+        "            np.array([r.iterations_run], float)]\n"
+        "np.save(sys.argv[1], np.concatenate(res))\n")
+    outs = []
+    for v in ("0", "1"):
+        out = tmp_path / f"o{v}.npy"
+        subprocess.run([sys.executable, str(script), str(out)], check=True,
+                       env=dict(os.environ, NDC_SPECULATE=v), timeout=600)
+        outs.append(np.load(out))
+    assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_plan_rl_leaves_observation(nd, oracle_c):
+    """deconv_rl on a plan clamps a copy: the resident observation is still the user's
+    (negative entries included) afterwards, and a PG run on the same plan matches a
+    fresh one."""
+    g = np.random.Generator(np.random.PCG64(11))
+    h = np.array([[0.05, 0.1, 0.05], [0.1, 0.4, 0.1], [0.05, 0.1, 0.05]])
+    y = g.uniform(-0.2, 1.0, (2, 14, 12)).astype(np.float32).astype(np.float64)
+    xs = (12, 10)
+    cfg = nd.DeconvConfig(max_iters=15, tol_rel_objective=0.0)
+    fresh = nd.deconv_pg_batch(y, h, xs, cfg)
+    with nd.Plan(xs, h, batch=2) as p:
+        p.set_observation(y)
+        p.rl_run(nd.RlConfig(max_iters=5))
+        for b in range(2):
+            rl = p.report(b, 6)
+            ref = nd.deconv_rl(y[b], h, xs, nd.RlConfig(max_iters=5))
+            assert np.array_equal(p.estimate()[b], ref.estimate)
+            assert rl.negative_pixels_clamped == ref.negative_pixels_clamped > 0
+        assert np.array_equal(p.observation(), y)
+        p.pg_run(cfg)
+        est = p.estimate()
+        for b in range(2):
+            assert np.array_equal(est[b], fresh[b].estimate)
+
+
+def test_power_iters_beyond_ring(nd):
+    """Any positive power_iters is accepted (solvers.hpp:127-143 has no cap): the device
+    iterations record lambdas in a 4096-slot ring.  Both device paths: float64 (small
+    problem) and float32 (|x| K > 2^28); the PSF is not rank-1, so neither takes the
+    separable host path."""
+    hh = np.outer(np.hanning(15)[1:-1] + 0.1, np.hanning(7)[1:-1] + 0.2)[:, :5]  # 13x5
+    hh[0, 0] += 0.05
+    hh /= hh.sum()
+    for xs in ((96, 80), (2048, 2048)):
+        s_long = nd.estimate_step(hh, xs, 4100)
+        s_ref = nd.estimate_step(hh, xs, 3000)
+        # lambda_k = ||A^T A v_k|| is non-decreasing for a PSD operator (Cauchy-Schwarz),
+        # so the longer run's step is at most the shorter one's (float32: to rounding)
+        assert np.isfinite(s_long) and s_ref * (1 - 1e-3) <= s_long <= s_ref * (1 + 1e-6), xs

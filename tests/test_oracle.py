@@ -140,3 +140,79 @@ def test_c_restatement_matches_reference_random():
             b = r.deconv_pg(yy, h, xs, max_iters=15, tol_rel_objective=0.0)
             assert np.array_equal(a.estimate, b.estimate)
             assert np.array_equal(a.objective_trace, b.objective_trace)
+
+
+# --- the threaded float64 oracle (oracle/ndconv_fast.c) used for config-scale parity ----
+
+@pytest.fixture(scope="module")
+def oracle_fast():
+    import os
+    o = Oracle("fast")
+    o.set_threads(os.cpu_count() or 1)
+    return o
+
+
+def _rel(a, b):
+    return float(np.linalg.norm((np.asarray(a) - b).ravel()) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def test_fast_oracle_operators(oracle_c, oracle_fast, golden_ops):
+    """Same sums in another order: every golden operator case and random 1-3-d shapes
+    (kernels larger than the input included) to 1e-13 relative."""
+    d = golden_ops
+    for i in range(int(d["n"])):
+        x, h = d[f"x{i}"], d[f"h{i}"]
+        if x.ndim > 3:
+            continue
+        assert _rel(oracle_fast.conv_full(x, h), d[f"y{i}"]) <= 1e-13, i
+        assert _rel(oracle_fast.adjoint_apply(d[f"r{i}"], h, x.shape), d[f"atr{i}"]) <= 1e-13, i
+    g = np.random.Generator(np.random.PCG64(2024))
+    for _ in range(60):
+        nd_ = int(g.integers(1, 4))
+        xs = tuple(int(v) for v in g.integers(1, 40 if nd_ < 3 else 12, nd_))
+        hs = tuple(int(2 * v + 1) for v in g.integers(0, 9 if nd_ < 3 else 4, nd_))
+        x, h = g.uniform(-1, 1, xs), g.uniform(-1, 1, hs)
+        y = oracle_c.conv_full(x, h)
+        assert _rel(oracle_fast.conv_full(x, h), y) <= 1e-13, (xs, hs)
+        r = g.uniform(-1, 1, y.shape)
+        assert _rel(oracle_fast.adjoint_apply(r, h, xs), oracle_c.adjoint_apply(r, h, xs)) <= 1e-13, (xs, hs)
+
+
+def test_fast_oracle_steps_and_pg(oracle_c, oracle_fast, golden_solvers):
+    """estimate_step and whole PG runs (golden family, config 1 with the auto step, the
+    KATs) against the bitwise oracle: steps to 1e-12, estimates / traces to 1e-10, same
+    iteration counts and stop reasons."""
+    d = golden_solvers
+    assert oracle_fast.estimate_step(np.array([2.0]), (5,), 10) == pytest.approx(float(d["step_h2"]), rel=1e-14)
+    assert oracle_fast.estimate_step(np.ones(3), (8,), 30) == pytest.approx(float(d["step_box"]), rel=1e-12)
+    n = int(d["npg"])
+    for i in list(range(n - 5)) + [n - 5, n - 4, n - 3, n - 1]:
+        kw = _pg_kwargs(d[f"pg_cfg{i}"])
+        xs = tuple(int(v) for v in d[f"pg_xs{i}"])
+        rep = oracle_fast.deconv_pg(d[f"pg_y{i}"], d[f"pg_h{i}"], xs, **kw)
+        assert rep.stop_reason == str(d[f"pg_stop{i}"]), i
+        n_it = int(d[f"pg_it{i}"])
+        tol = 1e-10 if rep.iterations_run == n_it else 1e-8
+        assert _rel(rep.estimate, d[f"pg_x{i}"]) <= tol or np.max(np.abs(rep.estimate - d[f"pg_x{i}"])) <= 1e-12, i
+        if rep.iterations_run != n_it:
+            # the bitwise fixed-point test trial == x (solvers.hpp:191) near a stalled
+            # optimum: a reordered sum may accept one more (or one fewer) tiny step
+            assert rep.stop_reason == "converged" and abs(rep.iterations_run - n_it) <= 2, i
+            m = min(rep.iterations_run, n_it) + 1
+            np.testing.assert_allclose(rep.objective_trace[:m], d[f"pg_obj{i}"][:m], rtol=1e-10)
+        else:
+            np.testing.assert_allclose(rep.objective_trace, d[f"pg_obj{i}"], rtol=1e-10, atol=1e-300)
+    assert rep.extra["step0"] == pytest.approx(float(d["c1_step"]), rel=1e-12)
+
+
+def test_fast_oracle_3d_pg(oracle_c, oracle_fast):
+    """A 3-D run with the config-3 PSF shape (31x15x15) on a small volume: whole PG run
+    equal to the bitwise oracle to 1e-10."""
+    from paper_1711_11224_b200 import synth
+    x, y, h = synth.make("c3", shape=(12, 16, 14), n_objects=6)
+    a = oracle_c.deconv_pg(y, h, x.shape, max_iters=8, tol_rel_objective=0.0)
+    b = oracle_fast.deconv_pg(y, h, x.shape, max_iters=8, tol_rel_objective=0.0)
+    assert a.iterations_run == b.iterations_run == 8
+    assert _rel(b.estimate, a.estimate) <= 1e-10
+    np.testing.assert_allclose(b.objective_trace, a.objective_trace, rtol=1e-10)
+    np.testing.assert_allclose(b.kkt_trace, a.kkt_trace, rtol=1e-8)
