@@ -25,7 +25,8 @@
  * Tensors have 1 to 3 dimensions (row-major, first index slowest, shape.hpp:55-64).
  * Both operators reduce to one row primitive, acc[o] += sum_j t[j] src[o + j]
  * (correlation form): the forward pass reads a zero-padded copy of x with reversed
- * tap rows, the adjoint reads r directly.  Threads split the output rows.
+ * tap rows, the adjoint reads r directly.  Threads split the output rows in blocks of
+ * kRows rows of one plane.
  */
 #include <math.h>
 #include <pthread.h>
@@ -52,12 +53,22 @@ void of_set_threads(int n) { g_threads = n < 1 ? 1 : (n > 256 ? 256 : n); }
 
 /* ---- row primitive ---------------------------------------------------------------- */
 
-/* acc[o] += sum_{j<k} t[j] * src[o + j] for o in [0, n).  Blocks of 32 outputs live in
- * registers across the tap loop (one load per FMA). */
+/* acc[o] += sum_{j<k} t[j] * src[o + j] for o in [0, n).  Blocks of 64 / 32 / 8 outputs
+ * live in registers across the tap loop (one load per FMA). */
 __attribute__((target_clones("avx512f", "avx2", "default")))
 static void row_corr(double* restrict acc, const double* restrict src, const double* restrict t, long n,
                      long k) {
   long o = 0;
+  for (; o + 64 <= n; o += 64) { /* 8 independent AVX-512 FMA chains: latency hidden */
+    double a[64];
+    for (int i = 0; i < 64; ++i) a[i] = acc[o + i];
+    for (long j = 0; j < k; ++j) {
+      const double tv = t[j];
+      const double* s = src + o + j;
+      for (int i = 0; i < 64; ++i) a[i] += tv * s[i];
+    }
+    for (int i = 0; i < 64; ++i) acc[o + i] = a[i];
+  }
   for (; o + 32 <= n; o += 32) {
     double a[32];
     for (int i = 0; i < 32; ++i) a[i] = acc[o + i];
@@ -152,19 +163,33 @@ typedef struct {
   double* y;
 } fwd_ctx;
 
-static void fwd_row(void* c, long row) {
+/* Work unit: kRows consecutive output rows of one plane, so every source row read for
+ * them is reused from L1 by each of the kRows accumulators it contributes to. */
+enum { kRows = 4 };
+
+static void fwd_rows(void* c, long unit) {
   const fwd_ctx* f = (const fwd_ctx*)c;
   const geo3* g = f->g;
-  const long oz = row / g->oy, oy = row % g->oy;
-  double* acc = f->y + (size_t)row * g->ox;
-  memset(acc, 0, (size_t)g->ox * sizeof(double));
+  const long per_plane = (g->oy + kRows - 1) / kRows;
+  const long oz = unit / per_plane, oy0 = (unit % per_plane) * kRows;
+  const long nr = g->oy - oy0 < kRows ? g->oy - oy0 : kRows;
+  double* acc0 = f->y + ((size_t)oz * g->oy + oy0) * g->ox;
+  memset(acc0, 0, (size_t)nr * g->ox * sizeof(double));
   const long jz0 = oz - g->mz + 1 > 0 ? oz - g->mz + 1 : 0, jz1 = oz < g->kz - 1 ? oz : g->kz - 1;
-  const long jy0 = oy - g->my + 1 > 0 ? oy - g->my + 1 : 0, jy1 = oy < g->ky - 1 ? oy : g->ky - 1;
-  for (long jz = jz0; jz <= jz1; ++jz)
-    for (long jy = jy0; jy <= jy1; ++jy) {
-      const double* src = f->xp + ((size_t)(oz - jz) * g->my + (oy - jy)) * f->px;
-      row_corr(acc, src, f->hrev + ((size_t)jz * g->ky + jy) * g->kx, g->ox, g->kx);
+  for (long jz = jz0; jz <= jz1; ++jz) {
+    const long iz = oz - jz;
+    /* source row iy feeds output row oy = iy + jy for every valid tap row jy */
+    const long iy0 = oy0 - (g->ky - 1) > 0 ? oy0 - (g->ky - 1) : 0;
+    const long iy1 = oy0 + nr - 1 < g->my - 1 ? oy0 + nr - 1 : g->my - 1;
+    for (long iy = iy0; iy <= iy1; ++iy) {
+      const double* src = f->xp + ((size_t)iz * g->my + iy) * f->px;
+      for (long r = 0; r < nr; ++r) {
+        const long jy = oy0 + r - iy;
+        if (jy < 0 || jy >= g->ky) continue;
+        row_corr(acc0 + (size_t)r * g->ox, src, f->hrev + ((size_t)jz * g->ky + jy) * g->kx, g->ox, g->kx);
+      }
     }
+  }
 }
 
 int of_conv_full(int ndim, const size_t* xext, const double* x, const size_t* hext, const double* h,
@@ -185,7 +210,7 @@ int of_conv_full(int ndim, const size_t* xext, const double* x, const size_t* he
   for (long r = 0; r < g.kz * g.ky; ++r)
     for (long j = 0; j < g.kx; ++j) hrev[r * g.kx + j] = h[r * g.kx + (g.kx - 1 - j)];
   fwd_ctx c = {&g, xp, px, hrev, y};
-  parallel_rows(g.oz * g.oy, fwd_row, &c);
+  parallel_rows(g.oz * ((g.oy + kRows - 1) / kRows), fwd_rows, &c);
   free(xp);
   free(hrev);
   return OF_OK;
@@ -200,16 +225,23 @@ typedef struct {
   double* out;
 } adj_ctx;
 
-static void adj_row(void* c, long row) {
+static void adj_rows(void* c, long unit) {
   const adj_ctx* a = (const adj_ctx*)c;
   const geo3* g = a->g;
-  const long z = row / g->my, yy = row % g->my;
-  double* acc = a->out + (size_t)row * g->mx;
-  memset(acc, 0, (size_t)g->mx * sizeof(double));
+  const long per_plane = (g->my + kRows - 1) / kRows;
+  const long z = unit / per_plane, y0 = (unit % per_plane) * kRows;
+  const long nr = g->my - y0 < kRows ? g->my - y0 : kRows;
+  double* acc0 = a->out + ((size_t)z * g->my + y0) * g->mx;
+  memset(acc0, 0, (size_t)nr * g->mx * sizeof(double));
   for (long jz = 0; jz < g->kz; ++jz)
-    for (long jy = 0; jy < g->ky; ++jy) {
-      const double* src = a->r + ((size_t)(z + jz) * g->oy + (yy + jy)) * g->ox;
-      row_corr(acc, src, a->h + ((size_t)jz * g->ky + jy) * g->kx, g->mx, g->kx);
+    /* source row sy feeds output row y = sy - jy */
+    for (long sy = y0; sy < y0 + nr + g->ky - 1; ++sy) {
+      const double* src = a->r + ((size_t)(z + jz) * g->oy + sy) * g->ox;
+      for (long r = 0; r < nr; ++r) {
+        const long jy = sy - (y0 + r);
+        if (jy < 0 || jy >= g->ky) continue;
+        row_corr(acc0 + (size_t)r * g->mx, src, a->h + ((size_t)jz * g->ky + jy) * g->kx, g->mx, g->kx);
+      }
     }
 }
 
@@ -221,7 +253,7 @@ int of_adjoint_apply(int ndim, const size_t* yext, const double* r, const size_t
   for (int i = 0; i < ndim; ++i)
     if (yext[i] != xext[i] + hext[i] - 1) return OF_SHAPE; /* convolution.hpp:169-172 */
   adj_ctx c = {&g, r, h, out};
-  parallel_rows(g.mz * g.my, adj_row, &c);
+  parallel_rows(g.mz * ((g.my + kRows - 1) / kRows), adj_rows, &c);
   return OF_OK;
 }
 

@@ -423,7 +423,9 @@ void Plan::h2d_staged(void* dev, const void* host, size_t bytes) {
   for (size_t off = 0; off < bytes; off += kPinChunk, ++i) {
     const int s = static_cast<int>(i & 1);
     const size_t n = std::min(kPinChunk, bytes - off);
-    if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    // the slot may still feed a DMA of this call or of an earlier one (any call starts
+    // at slot 0): wait for its last use before the host overwrites it
+    check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
     par_copy(hpin_[s], static_cast<const char*>(host) + off, n);
     check_cuda(cudaMemcpyAsync(static_cast<char*>(dev) + off, hpin_[s], n, cudaMemcpyHostToDevice,
                                stream_),
@@ -841,7 +843,9 @@ void Plan::h2d_f64_as_f32(float* dev, const double* host, size_t n) {
   for (size_t off = 0; off < n; off += chunk, ++i) {
     const int s = static_cast<int>(i & 1);
     const size_t m = std::min(chunk, n - off);
-    if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+    // the slot may still feed a DMA of this call or of an earlier one (any call starts
+    // at slot 0): wait for its last use before the host overwrites it
+    check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
     par_convert(static_cast<float*>(hpin_[s]), host + off, m);
     check_cuda(cudaMemcpyAsync(dev + off, hpin_[s], m * 4, cudaMemcpyHostToDevice, stream_), "H2D");
     check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
@@ -1190,7 +1194,7 @@ void Plan::load_observation_ndtensor(const std::string& path) {
     for (size_t off = 0; off < own; off += chunk, ++i) {
       const int s = static_cast<int>(i & 1);
       const size_t n = std::min(chunk, own - off);
-      if (i >= 2) check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
+      check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");  // the slot's last DMA
       double* buf = static_cast<double*>(hpin_[s]);
       bool io_ok = true;
       const size_t bad = chunk_io(false, fd.fd, buf, n, h.payload_offset + (first + off) * 8, io_ok);

@@ -371,3 +371,23 @@ def test_power_iters_beyond_ring(nd):
         # lambda_k = ||A^T A v_k|| is non-decreasing for a PSD operator (Cauchy-Schwarz),
         # so the longer run's step is at most the shorter one's (float32: to rounding)
         assert np.isfinite(s_long) and s_ref * (1 - 1e-3) <= s_long <= s_ref * (1 + 1e-6), xs
+
+
+def test_large_batch_uploads_match_single_images(nd):
+    """Batches whose images exceed the 4 MB direct-copy limit go through the pinned
+    staging ring image by image (f64 -> f32 conversion on the host pool): every image of
+    the batch equals its own single-image run bit for bit, so no ring slot is
+    overwritten while an earlier image's DMA still reads it."""
+    g = np.random.Generator(np.random.PCG64(12))
+    h = np.outer(np.hanning(9)[1:-1], np.hanning(9)[1:-1])
+    h /= h.sum()
+    xs = (1100, 1000)
+    y = g.uniform(0, 1, (5,) + nd.conv_output_shape(xs, h)).astype(np.float32).astype(np.float64)
+    cfg = nd.DeconvConfig(max_iters=3, tol_rel_objective=0.0, initial_step=1.0)
+    reps = nd.deconv_pg_batch(y, h, xs, cfg)
+    for b in (0, 2, 4):
+        one = nd.deconv_pg(y[b], h, xs, cfg)
+        assert np.array_equal(reps[b].estimate, one.estimate), b
+    yb = nd.conv_full_batch(y[:, :xs[0], :xs[1]].astype(np.float32), h)
+    for b in (1, 3):
+        assert np.array_equal(yb[b], nd.conv_full_batch(y[b:b + 1, :xs[0], :xs[1]].astype(np.float32), h)[0]), b
