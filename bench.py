@@ -1,21 +1,31 @@
 """Benchmark of the convolution-only deconvolution hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
 
 Metric (BASELINE.json): voxel-iterations/s of the projected-gradient iteration (forward
-full conv + residual + adjoint valid correlation + projected update + reductions).
-A "step" is one PG iteration over one batch: config 2 = 16 independent 2048x2048
-images, 31x31 Gaussian PSF (sigma 4), Poisson noise at peak 1000.  Inputs are seeded
-synthetic data of exactly that shape (no dataset exists); they are resident in HBM
-before the timed region and, at 16 x 2048^2 fp32 (>= 268 MB per tensor), larger than
-the 126 MB L2, so no flush is needed between steps.
+full conv + residual + adjoint valid correlation + projected update + reductions) and
+its fraction of the FP32 roofline, at 1/2/4/8 B200.
 
-One JSON line on rank 0.  `value` is device time (CUDA events on the plan's stream,
-max over ranks); `e2e` is the same metric through the public C-ABI call with host f64
-buffers (H2D of Y, power-iteration step estimate, all iterations, D2H of the estimate
-and traces inside the timed region); `roofline` is the dominant kernel's algorithmic
-FLOP rate against the FP32 FFMA peak; `cpu_baseline` is the reference (oracle/_ref,
-the unmodified reference compiled from /root/reference) on this host's cores.
+Default workload, at every N: BASELINE config 5 -- the largest 3-D volume, 256 x 2048 x
+2048 voxels (1.07 G), the 65x33x33 widefield 3-Gaussian PSF (70,785 taps), filaments +
+5000 blobs, Poisson noise at peak 200, 20 iterations -- the config north_star's ">= 85 %
+parallel efficiency at 8 GPUs on the largest 3D volume" names.  At N = 1 it runs on one
+GPU; at N > 1 the volume is z-slab sharded across the N ranks (p_z = 32-plane halos over
+NCCL, rank-order scalar combine), so `scaling` is "strong" (the total volume is fixed)
+and BENCH N=1 is SCALE N=1.  Every rank generates only its own slab's observation (the
+x planes it depends on, seeded per object and per plane, bit-identical to the full
+volume's planes).  `--config c2` (16 x 2048^2 images, 31x31 PSF; N > 1 = independent
+replicas), c3, c4 and c2s (small-PSF HBM case) select the other configs.
+
+A "step" is one PG iteration over the whole volume (or batch).  Inputs are resident in
+HBM before the timed region and larger than the 126 MB L2 (no flush needed).  One JSON
+line on rank 0.  `value` is device time (CUDA events on the plan's stream, max over
+ranks); `e2e` is the same metric through the public C-ABI with host f64 buffers: the
+upload of the observation, a whole deconv_pg run of the config's iteration count, the
+download of the estimate and traces inside the timed region (max over ranks);
+`roofline` is the dominant pass's algorithmic FLOP rate against the FP32 FFMA peak;
+`cpu_baseline` is the reference (oracle/_ref, the unmodified reference compiled from
+/root/reference) on this host's cores.
 """
 from __future__ import annotations
 
@@ -36,17 +46,17 @@ N_SM = 148
 FFMA_PER_SM_CLK = 128
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="timed PG iterations (default per config)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=2)
-    return ap.parse_args()
+    ap.add_argument("--cpu-iters", type=int, default=1)
+    return ap.parse_args(argv)
 
 
 # --- distributed plumbing -------------------------------------------------------------------
@@ -62,7 +72,14 @@ class Dist:
     def __init__(self, backend="nccl"):
         self.rank, self.world, self.local = dist_env()
         self.pg = None
+        self.backend = backend
         if self.world > 1:
+            if backend == "nccl":
+                # communicator lines (rank, nranks, transport) for the run log, on stderr so
+                # the JSON line stays the only line on stdout
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -73,13 +90,21 @@ class Dist:
             self.torch = torch
 
     def barrier(self):
+        """Device-wide sync first (no plan NCCL operation is in flight when the plumbing
+        communicator's barrier runs), then the rank barrier."""
         if self.world > 1:
+            if self.backend == "nccl":
+                self.torch.cuda.synchronize()
             self.dist.barrier()
+
+    def allmax(self, v: float) -> float:
+        return self.max(v)
 
     def max(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -163,15 +188,17 @@ class Clocks:
 
 # --- workloads --------------------------------------------------------------------------------
 
-# Per-config defaults: iterations per e2e call, timed steps, explicit step size.  Configs
-# 4/5 use initial_step = 1 (their PSFs are nonnegative with unit sum, so ||A|| <= 1 and
-# 1 is a valid gradient step; it skips a power iteration costing 60 passes = 30 PG
-# iterations of compute); configs 2/3 estimate the step (untimed setup).
+# Per-config defaults: iterations per e2e solve (the config's BASELINE iteration count),
+# timed steps, explicit step size.  The 3-D configs use initial_step = 1 (their PSFs
+# are nonnegative with unit sum, so ||A|| <= 1 and 1 is a valid gradient step; the auto
+# step at these sizes is checked against the reference in tests/test_gpu_config_scale.py);
+# the 2-D batches estimate the step (untimed setup).
 WORK = {
     "c2": dict(e2e_iters=100, steps=30, step=None, desc="16x2048x2048 2D batch, PSF 31x31 sigma 4, Poisson 1000"),
-    "c3": dict(e2e_iters=50, steps=20, step=None, desc="3D 256x256x128, PSF 15x15x31 sigma_xy 1.5 sigma_z 4"),
+    "c3": dict(e2e_iters=50, steps=20, step=1.0, desc="3D 256x256x128, PSF 15x15x31 sigma_xy 1.5 sigma_z 4"),
     "c4": dict(e2e_iters=30, steps=5, step=1.0, desc="3D 1024x1024x512, PSF 9x9x21, Poisson 500"),
-    "c5": dict(e2e_iters=2, steps=2, step=1.0, desc="3D 2048x2048x256, 33x33x65 3-Gaussian PSF, Poisson 200"),
+    "c5": dict(e2e_iters=20, steps=3, step=1.0,
+               desc="3D 2048x2048x256 (filaments + 5000 blobs), 33x33x65 3-Gaussian widefield PSF, Poisson 200"),
     # HBM-bound small-PSF case (not a BASELINE config; north_star's ">= 70 % HBM" target)
     "c2s": dict(e2e_iters=100, steps=500, step=None,
                 desc="16x2048x2048 2D batch, PSF 5x5 sigma 1 (reference acceptance PSF), Poisson 1000"),
@@ -179,16 +206,31 @@ WORK = {
 HBM_BOUND = ("c2s",)
 
 
-def inputs(config: str, rank: int, sharded: bool):
-    """x (B, ...), y (B, ...) float32-exact and the PSF.  2-D batches get a different
-    seed per rank (independent replicas); a sharded 3-D volume is the same on every rank
-    (each keeps its own z-slab)."""
+VOLUME = ("c3", "c4", "c5")
+
+
+def inputs_2d(config: str, rank: int):
+    """A 2-D batch (independent images; each rank of a replica run its own seed)."""
     from paper_1711_11224_b200 import synth
-    seed = synth.SEED if sharded else synth.SEED + 100003 * rank
-    x, y, h = synth.make(config, seed=seed)
-    if x.ndim == len(h.shape):  # single volume -> batch of one
-        x, y = x[None], y[None]
-    return x.astype(np.float32), y.astype(np.float32), h
+    _, y, h = synth.make(config, seed=synth.SEED + 100003 * rank)
+    return y.astype(np.float32), h
+
+
+def inputs_volume(config: str, y0: int, y1: int, d, device, shape=None, n_objects=None):
+    """Observation planes [y0, y1) of a 3-D config, float32: the rank generates the x
+    planes they depend on (synth.clean_observation_planes), the noise is seeded per plane
+    and scaled by the whole volume's maximum (all-reduced), so every plane equals the
+    unsharded volume's."""
+    from paper_1711_11224_b200 import synth
+    yc = synth.clean_observation_planes(config, y0, y1, shape=shape, n_objects=n_objects)
+    if config == "c3":
+        y = synth.gaussian_planes(yc, 0.005, synth.SEED + 1000, y0)
+    else:
+        peak = {"c4": 500.0, "c5": 200.0}[config]
+        m = d.allmax(float(yc.max()))
+        y = synth.poisson_planes(yc, peak, m, synth.SEED + 1000, y0, device=device)
+    del yc
+    return y.astype(np.float32)[None]
 
 
 # --- CPU baseline (reference compiled from /root/reference: oracle/_ref) --------------------
@@ -271,22 +313,32 @@ def run_ours(a):
     rank, world, local = dist_env()
     d = Dist("nccl")
     import torch  # plumbing only: external-stream CUDA events and the rank collectives
-    from paper_1711_11224_b200 import ndconv as nd
+    from paper_1711_11224_b200 import ndconv as nd, synth
     if nd.device_count() < 1:
         raise SystemExit("no B200 visible")
+    torch.cuda.set_device(local)
     work = WORK[a.config]
     steps = a.steps if a.steps is not None else work["steps"]
-    sharded = world > 1 and a.config in ("c3", "c4", "c5")
-    x, y, h = inputs(a.config, rank, sharded)
-    B = y.shape[0]
-    x_shape = x.shape[1:]
+    volume = a.config in VOLUME
+    sharded = world > 1 and volume
+    t_gen = time.perf_counter()
+    if volume:
+        x_shape = tuple(synth.CONFIGS[a.config]["shape"])
+        h = synth.psf_for(a.config)
+        B = 1
+        _, _, ya, yb = nd.slab_range(x_shape[0], (h.shape[0] - 1) // 2, rank, world) if sharded \
+            else (0, 0, 0, x_shape[0] + h.shape[0] - 1)
+        y_own = inputs_volume(a.config, ya, yb, d, f"cuda:{local}")
+    else:
+        y_own, h = inputs_2d(a.config, rank)
+        B = y_own.shape[0]
+        x_shape = tuple(s - k + 1 for s, k in zip(y_own.shape[1:], h.shape))
+    t_gen = time.perf_counter() - t_gen
     K = int(np.prod(h.shape))
     plan = make_plan(nd, d, x_shape, h, B, local, sharded)
-    ya, yb = plan.y_range
-    xa, xb = plan.x_range
-    y_own = y[:, ya:yb] if sharded else y
-    vox_rank = B * (xb - xa) * int(np.prod(x_shape[1:])) if sharded else B * int(np.prod(x_shape))
-    vox_job = B * int(np.prod(x_shape)) * (1 if sharded else world)
+    xa, xb = plan.x_range if sharded else (0, x_shape[0])
+    vox_rank = B * (xb - xa) * int(np.prod(x_shape[1:]))
+    vox_job = B * int(np.prod(x_shape)) * (1 if (sharded or volume) else world)
     cfg = nd.DeconvConfig(max_iters=a.warmup + steps + 1, tol_rel_objective=0.0, initial_step=work["step"])
 
     plan.set_observation(y_own)
@@ -295,7 +347,6 @@ def run_ours(a):
     clocks.start()  # sampling runs through warm-up and the timed steps
     for _ in range(a.warmup):
         plan.pg_iterate(1)
-    torch.cuda.set_device(local)
     stream = torch.cuda.ExternalStream(plan.stream(), device=f"cuda:{local}")
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -320,13 +371,12 @@ def run_ours(a):
     plan.set_timing(False)
     plan.pg_end()
     rep = plan.report(0, cfg.max_iters + 1)
-    plan.close()
 
     value = vox_job * steps / (ms_max / 1e3)
-    # Dominant kernel: algorithmic FLOPs per pass = 2 K per x voxel of this rank (forward:
+    # Dominant pass: algorithmic FLOPs per pass = 2 K per x voxel of this rank (forward:
     # every x voxel meets K taps; adjoint: every output meets K taps).  A pass is one
     # launch, or several tap-chunk launches for PSFs beyond the 7680-tap parameter block
-    # (config 5) -- the roofline uses the pass time.
+    # (config 5: 11) -- the roofline uses the pass time.
     flops_pass = 2.0 * K * vox_rank
     passes = steps  # one forward and one adjoint per accepted iteration without backtracks
     dom, n_dom, ms_dom = ("adjoint", n_adj, ms_adj) if ms_adj >= ms_fwd else ("forward", n_fwd, ms_fwd)
@@ -347,19 +397,22 @@ def run_ours(a):
             traffic = json.load(open(tf)).get(a.config, {}).get(dom)
         except (OSError, ValueError):
             traffic = None
+    par = "single" if world == 1 else (f"z-slab{world}" if sharded else f"replicas{world}")
     line = {
         "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
         "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": steps,
         "warmup": a.warmup, "ms_per_step": ms_max / steps, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if volume else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"{a.config}: {work['desc']}",
                    "batch_per_gpu": B, "x_shape": list(x_shape), "psf": list(h.shape), "taps": K,
-                   "parallelism": (f"z-slab{world}" if sharded else f"replicas{world}") if world > 1 else "single",
-                   "l2": "inputs larger than L2 (no flush)", "step": "one PG iteration over the batch",
+                   "parallelism": par, "x_planes_per_rank": xb - xa if volume else None,
+                   "l2": "inputs larger than L2 (no flush)",
+                   "step": "one PG iteration over the whole " + ("volume" if volume else "batch"),
                    "tol_rel_objective": 0.0,
                    "step_size": "auto (power iteration, untimed setup)" if work["step"] is None
-                   else f"initial_step={work['step']} (unit-sum PSF)"},
+                   else f"initial_step={work['step']} (unit-sum PSF)",
+                   "input_generation_s": round(t_gen, 2)},
         "roofline": ({"bound": "hbm", "kernel": dom, "achieved": bytes_pass / avg_s / 1e9, "peak": hbm_peak[0],
                       "unit": "GB/s", "frac": bytes_pass / avg_s / 1e9 / hbm_peak[0], "traffic": traffic,
                       "peak_basis": hbm_peak[1], "algorithmic_bytes_per_pass": bytes_pass,
@@ -381,8 +434,12 @@ def run_ours(a):
         "iterations_accepted": int(rep.iterations_run),
         "backtracks": int(rep.extra.get("backtracks", 0)),
     }
-    if not a.no_e2e and not sharded:
-        line["e2e"] = e2e(a, nd, y, h, x_shape, B, work, world, d)
+    if not a.no_e2e:
+        if volume:
+            line["e2e"] = e2e_plan(nd, plan, y_own, work, vox_job, d)
+        else:
+            line["e2e"] = e2e_batch(nd, y_own, h, x_shape, B, work, world, d)
+    plan.close()
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cb, _ = cpu_reference_sample(a.config, a.cpu_iters)
         line["cpu_baseline"] = cb
@@ -391,7 +448,30 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
 
 
-def e2e(a, nd, y32, h, x_shape, B, work, world, d):
+def e2e_plan(nd, plan, y32, work, vox_job, d):
+    """The public plan C-ABI with host f64 buffers, one whole solve per step: upload of
+    this rank's observation planes (f64 -> f32 on the host pool, pinned ring, H2D),
+    deconv_pg over the config's iteration count (ndc_plan_pg_run), download of the
+    estimate planes as f64 and of the traces.  Max over ranks."""
+    iters = work["e2e_iters"]
+    yh = np.ascontiguousarray(y32, dtype=np.float64)
+    cfg = nd.DeconvConfig(max_iters=iters, tol_rel_objective=0.0, initial_step=work["step"])
+    d.barrier()
+    t0 = time.perf_counter()
+    plan.set_observation(yh)
+    plan.pg_run(cfg)
+    x = plan.estimate()
+    rep = plan.report(0, iters + 1)
+    dt = d.max(time.perf_counter() - t0)
+    return {"value": vox_job * iters / dt, "unit": "voxel-iterations/s",
+            "h2d_bytes_per_step": int(yh.nbytes),
+            "d2h_bytes_per_step": int(x.nbytes + rep.objective_trace.nbytes + rep.kkt_trace.nbytes),
+            "step": f"one full deconv_pg solve through the plan C-ABI (set_observation_f64, pg_run, "
+                    f"get_estimate_f64, get_report): {iters} iterations, initial_step={work['step']}",
+            "seconds_per_step": dt, "iterations_run": int(rep.iterations_run)}
+
+
+def e2e_batch(nd, y32, h, x_shape, B, work, world, d):
     """Public C-ABI call (ndc_deconv_pg_batch_f64) with host f64 buffers: a whole solve
     per step -- H2D of Y, step estimate, all iterations, D2H of estimate and traces."""
     import ctypes as C

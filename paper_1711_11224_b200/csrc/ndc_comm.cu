@@ -1,7 +1,13 @@
 // z-slab transports (ndc_plan.h Transport):
 //  * NcclTransport -- one process per GPU, grouped ncclSend/ncclRecv for the p_z-plane
-//    halos (on a split communicator: the plan runs them on its comm stream, overlapped
-//    with compute) and ncclAllGather for the per-rank f64 partials, over NVLink / NVSwitch.
+//    halos (the plan issues them on its comm stream, overlapped with compute) and
+//    ncclAllGather for the per-rank f64 partials (plan stream), over NVLink / NVSwitch.
+//    Both go through ONE communicator: NCCL runs the operations of a communicator in
+//    the order they are issued, whatever user stream each is enqueued on, and every rank
+//    issues the same sequence (identical host decisions), so the order is the same on
+//    all ranks -- no cross-communicator ordering hazard.  The price is that a scalar
+//    all-gather waits for a halo exchange issued before it (config 5 at 8 ranks: ~0.6 ms
+//    of NVLink time against a ~0.6 s iteration).
 //    libnccl.so.2 is opened at run time (the unsharded path never needs it; when torch
 //    has already loaded its bundled NCCL the same library object is reused).
 //  * LocalTransport -- several slab ranks driven by host threads of one process (tests
@@ -26,7 +32,6 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -47,7 +52,6 @@ NcclApi& nccl() {
     api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
-    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(dlsym(h, "ncclCommSplit"));
     api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
@@ -78,17 +82,8 @@ class NcclTransport final : public Transport {
     static_assert(sizeof(uid.internal) == 128, "ncclUniqueId size");
     std::memcpy(uid.internal, id, 128);
     check_nccl(nccl().CommInitRank(&comm_, world, uid, rank), "ncclCommInitRank");
-    // Halo send/recv get their own communicator: the plan issues them on its comm stream,
-    // overlapped with compute and with the scalar all-gathers on the plan stream, and
-    // operations of ONE communicator would be serialised in issue order.
-    halo_comm_ = comm_;
-    if (nccl().CommSplit) {
-      ncclComm_t c = nullptr;
-      if (nccl().CommSplit(comm_, 0, rank, &c, nullptr) == ncclSuccess && c) halo_comm_ = c;
-    }
   }
   ~NcclTransport() override {
-    if (halo_comm_ && halo_comm_ != comm_ && nccl().CommDestroy) nccl().CommDestroy(halo_comm_);
     if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   }
   int rank() const override { return rank_; }
@@ -97,10 +92,10 @@ class NcclTransport final : public Transport {
                 size_t count, cudaStream_t s) override {
     auto& api = nccl();
     check_nccl(api.GroupStart(), "ncclGroupStart");
-    if (send_lo) check_nccl(api.Send(send_lo, count, ncclFloat32, rank_ - 1, halo_comm_, s), "ncclSend");
-    if (recv_lo) check_nccl(api.Recv(recv_lo, count, ncclFloat32, rank_ - 1, halo_comm_, s), "ncclRecv");
-    if (send_hi) check_nccl(api.Send(send_hi, count, ncclFloat32, rank_ + 1, halo_comm_, s), "ncclSend");
-    if (recv_hi) check_nccl(api.Recv(recv_hi, count, ncclFloat32, rank_ + 1, halo_comm_, s), "ncclRecv");
+    if (send_lo) check_nccl(api.Send(send_lo, count, ncclFloat32, rank_ - 1, comm_, s), "ncclSend");
+    if (recv_lo) check_nccl(api.Recv(recv_lo, count, ncclFloat32, rank_ - 1, comm_, s), "ncclRecv");
+    if (send_hi) check_nccl(api.Send(send_hi, count, ncclFloat32, rank_ + 1, comm_, s), "ncclSend");
+    if (recv_hi) check_nccl(api.Recv(recv_hi, count, ncclFloat32, rank_ + 1, comm_, s), "ncclRecv");
     check_nccl(api.GroupEnd(), "ncclGroupEnd");
   }
   void allgather(const double* in, double* out, size_t n, cudaStream_t s) override {
@@ -110,7 +105,6 @@ class NcclTransport final : public Transport {
  private:
   int rank_, world_;
   ncclComm_t comm_ = nullptr;
-  ncclComm_t halo_comm_ = nullptr;  // == comm_ when ncclCommSplit is unavailable
 };
 
 }  // namespace

@@ -497,7 +497,7 @@ void Plan::alloc_all() {
   dscale_ = static_cast<float*>(dmalloc(B_ * sizeof(float)));
   dactive_ = static_cast<int*>(dmalloc(B_ * sizeof(int)));
   dstep_ = static_cast<double*>(dmalloc(B_ * sizeof(double)));
-  if (world_ > 1) gather_ = static_cast<double*>(dmalloc(2 * world_ * sizeof(double)));
+  if (comm_) gather_ = static_cast<double*>(dmalloc(2 * world_ * sizeof(double)));
   std::vector<float> ones(B_, 1.0f);
   check_cuda(cudaMemcpyAsync(dscale_, ones.data(), B_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
   std::vector<int> act(B_, 1);
@@ -726,14 +726,15 @@ KernelStats Plan::stats(int kind) {
 
 void Plan::finalize(long long per_image, int op, double* out0, double* out1, float* scale_out,
                     const int* active) {
-  if (world_ == 1) {
+  if (!comm_) {
     check_cuda(launch_finalize(partials_, per_image, static_cast<int>(B_), op, out0, out1, scale_out,
                                active, stream_),
                "finalize launch");
     st_[2].launches++;
     return;
   }
-  // z-slab ranks: raw local reduction -> all-gather (rank order) -> identical combine.
+  // z-slab ranks: raw local reduction -> all-gather (rank order) -> identical combine
+  // (a one-rank transport runs the same sequence: its all-gather is a real NCCL call).
   const int raw = (op == kFinMaxSum) ? kFinMaxSum : kFinSumSum;
   double* gin = dsc_ + kNumSlots * B_ + kMaxPowerIters;  // 2 doubles
   double* gout = gather_;                                 // 2 * world doubles

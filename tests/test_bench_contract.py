@@ -19,7 +19,7 @@ def _run(*args, timeout=600):
 
 @pytest.mark.skipif(not os.path.exists(REF_LIB), reason="oracle/_ref not built")
 def test_reference_arm_line():
-    p = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
+    p = _run("--impl", "reference", "--config", "c2", "--steps", "1", "--warmup", "3")
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, p.stdout
@@ -45,3 +45,13 @@ def test_product_arm_fails_loudly_without_gpu():
     p = _run("--steps", "1", "--warmup", "3", timeout=300)
     assert p.returncode != 0
     assert not [l for l in p.stdout.splitlines() if l.startswith("{") and '"value"' in l]
+
+
+def test_default_workload_is_config5_at_every_n():
+    """north_star's scaling target is config 5 (the largest 3-D volume): the default
+    workload for every N, z-slab sharded when N > 1 (BENCH N=1 == SCALE N=1)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    a = bench.parse([])
+    assert a.config == "c5" and a.gpus == 1 and a.warmup >= 3
+    assert bench.WORK["c5"]["e2e_iters"] == 20 and "c5" in bench.VOLUME

@@ -146,3 +146,51 @@ def test_slab_halo_decomposition_gloo(world):
         p.join(timeout=240)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=10) is True
+
+
+def _gen_worker(rank, world, port, q):
+    """bench.py's per-rank observation generation (inputs_volume over gloo: the volume
+    maximum all-reduced, noise seeded per plane) -- each rank only its own y planes."""
+    import sys
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"], os.environ["WORLD_SIZE"], os.environ["LOCAL_RANK"] = str(rank), str(world), str(rank)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_1711_11224_b200 import ndconv as nd
+    d = bench.Dist("gloo")
+    try:
+        shape, nobj = (40, 30, 34), 60
+        for cfg in ("c4", "c5"):
+            kz = {"c4": 21, "c5": 65}[cfg]
+            if cfg == "c5":
+                shape = (72, 20, 22)
+            _, _, ya, yb = nd.slab_range(shape[0], (kz - 1) // 2, rank, world)
+            mine = bench.inputs_volume(cfg, ya, yb, d, None, shape=shape, n_objects=nobj)[0]
+            objs = [None] * world
+            dist.all_gather_object(objs, (ya, mine))
+            if rank == 0:
+                got = np.concatenate([o[1] for o in sorted(objs, key=lambda o: o[0])], axis=0)
+                d1 = bench.Dist.__new__(bench.Dist)
+                d1.world = 1
+                whole = bench.inputs_volume(cfg, 0, shape[0] + kz - 1, d1, None, shape=shape, n_objects=nobj)[0]
+                q.put((cfg, got.shape == whole.shape and np.array_equal(got, whole)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_per_rank_inputs_gloo():
+    """Two ranks' generated observation planes assemble to the single-rank volume bit for
+    bit (configs 4 and 5 generators, Poisson noise on the host fallback)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gen_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {"c4": True, "c5": True}, res
