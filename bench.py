@@ -383,7 +383,14 @@ def run_ours(a):
     avg_s = ms_dom / max(passes, 1) / 1e3
     achieved = flops_pass / avg_s / 1e12
     smax = clk.get("sm_max_mhz") or 1965.0
-    peak = N_SM * FFMA_PER_SM_CLK * 2 * smax * 1e6 / 1e12
+    peak_theory = N_SM * FFMA_PER_SM_CLK * 2 * smax * 1e6 / 1e12
+    # measured FP32 FMA peak on this GPU, right after the timed region (same clocks):
+    # a register-only packed-FMA kernel on every SM (ndc_probe_fp32_peak)
+    try:
+        peak_meas = nd.probe_fp32_peak(local)
+    except nd.Error:
+        peak_meas = None
+    peak = peak_meas or peak_theory
     if a.config in HBM_BOUND:
         # algorithmic bytes per pass (float32): forward reads x and Y, writes r; adjoint
         # reads r and x, writes trial and g (Plan PG passes)
@@ -422,8 +429,11 @@ def run_ours(a):
                      if a.config in HBM_BOUND else
                      {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_basis": f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (sm max clock); "
-                                   "no measured FP32 peak in MEASURED_PEAKS.json",
+                     "peak_basis": ("measured on this GPU after the timed region: register-only FFMA2 "
+                                    "probe on all SMs (ndc_probe_fp32_peak); MEASURED_PEAKS.json has no "
+                                    "FP32 figure" if peak_meas else
+                                    f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (probe unavailable)"),
+                     "peak_theoretical": peak_theory, "frac_theoretical": achieved / peak_theory,
                      "algorithmic_flops_per_pass": flops_pass, "pass_ms": avg_s * 1e3,
                      "launches_per_pass": n_dom / max(passes, 1),
                      "frac_at_observed_clock": (achieved / (N_SM * FFMA_PER_SM_CLK * 2 * clk["sm_mhz"] * 1e6 / 1e12)

@@ -245,6 +245,9 @@ ndc_status ndc_plan_set_timing(ndc_plan* plan, int enabled);
 ndc_status ndc_plan_reset_stats(ndc_plan* plan);
 ndc_status ndc_plan_stats(ndc_plan* plan, int kind, uint64_t* launches, double* total_ms);
 ndc_status ndc_plan_stream(ndc_plan* plan, void** cuda_stream);
+/* Measured FP32 FMA throughput of `device` in TFLOP/s (best of 4 runs of a register-only
+ * packed-FMA kernel on every SM): the roofline denominator the bench reports against. */
+ndc_status ndc_probe_fp32_peak(int device, double* tflops);
 
 /* ---- z-slab sharding across processes (one GPU per rank, NCCL over NVLink) ----
  * Rank r of `world` owns x planes [a_r, b_r) of the slowest axis (ndc_slab_range)

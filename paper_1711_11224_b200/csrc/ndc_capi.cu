@@ -600,6 +600,13 @@ ndc_status ndc_plan_create_sharded(ndc_plan** plan, int device, int ndim, const 
   });
 }
 
+ndc_status ndc_probe_fp32_peak(int device, double* tflops) {
+  return guard([&] {
+    need(tflops, "tflops");
+    *tflops = ndc::probe_fp32_peak(device);
+  });
+}
+
 ndc_status ndc_nccl_unique_id(unsigned char id[128]) {
   return guard([&] {
     need(id, "id");

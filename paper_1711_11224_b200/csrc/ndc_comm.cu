@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -45,7 +46,12 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    // NDC_NCCL_LIBRARY: an explicit libnccl path (a process that will also load another
+    // NCCL -- e.g. a framework's bundled copy -- must use that same library: the dynamic
+    // linker shares one libnccl.so.2 per process by soname)
+    void* h = nullptr;
+    if (const char* path = std::getenv("NDC_NCCL_LIBRARY")) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!h) return;
     api.lib = h;

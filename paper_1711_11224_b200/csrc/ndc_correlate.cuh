@@ -67,26 +67,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Edge-tile tap-row split by a uniform loop with per-warp skips (see accumulate_rows).
-#ifndef NDC_EDGE_UNIFORM
-#define NDC_EDGE_UNIFORM 0
-#endif
-
 // Output-plane-fastest CTA order for 3-D launches (see correlate_kernel).  Measured
 // (profiles/r01m_kbench_z_fast.txt): config 4 forward DRAM reads 35.9 -> 5.1 GB per pass
 // (the KZ = 21 input planes of a tile stay in L2); step times equal within 0.3 %.
 #ifndef NDC_Z_FAST
 #define NDC_Z_FAST 1
 #endif
-
-// L2 prefetch of the two 32-byte sectors of a 64-byte row segment (no register result).
-#ifndef NDC_L2_PREFETCH
-#define NDC_L2_PREFETCH 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const float* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 8));
-}
 
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -421,13 +407,6 @@ __device__ __forceinline__ void row_value(const RowAcc<true>& r, float (&o)[kRX]
   o[kRX - 1] += r.b15;
 }
 
-// Tap-row loop unroll (a tuning knob; measured: 2 or 3 costs 10-30 % on configs 2-4 --
-// the unrolled body no longer keeps the taps on the uniform datapath).
-#ifndef NDC_KY_UNROLL
-#define NDC_KY_UNROLL 1
-#endif
-constexpr int kKyUnroll = NDC_KY_UNROLL;
-
 // NR of the thread's RY row windows against every tap row of one staged plane.
 template <int KX, int SH, int RY, int NR, bool STRIDED, bool PK>
 __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const float* base,
@@ -437,18 +416,13 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
   constexpr int KXP = tap_pitch(KX);
   // Tap rows 0..KY-1 (STRIDED, edge tiles only: ky0, ky0 + kys, ...).  In the interior
   // kernel the induction variable is uniform, which keeps the tap loads on the uniform
-  // datapath (LDCU -> FFMA R, R, UR).
-#pragma unroll kKyUnroll
-  for (int ky = (STRIDED && !NDC_EDGE_UNIFORM) ? ky0 : 0; ky < KY; ky += (STRIDED && !NDC_EDGE_UNIFORM) ? kys : 1) {
-    // edge tiles (NDC_EDGE_UNIFORM): walk every tap row with a uniform induction variable
-    // (taps stay on the uniform datapath) and skip the rows of the other phases
-    if (STRIDED && NDC_EDGE_UNIFORM && ky % kys != ky0) continue;
-    const float* w = trow + ky * KXP;
-#if defined(NDC_J_NOUNROLL)
+  // datapath (LDCU -> FFMA R, R, UR).  Measured and not kept: unrolling this
+  // loop (taps leave the uniform datapath, -10..30 %), a uniform loop with per-phase skips
+  // for edge tiles (+3 % on config 3's forward).
 #pragma unroll 1
-#else
+  for (int ky = STRIDED ? ky0 : 0; ky < KY; ky += STRIDED ? kys : 1) {
+    const float* w = trow + ky * KXP;
 #pragma unroll
-#endif
     for (int j = 0; j < NR; ++j) {
       const float* rp = base + (ky + 32 * j) * pitch_s;
       float win[NQ * 4];
@@ -643,27 +617,6 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
       mbar_expect_tx(&bars[i], tx_bytes);
       tma_load_3d(smem_raw + i * sbytes, &map, &bars[i], tx0 + g.off_x, ty0 + g.off_y,
                   b * g.in_ez + iz);
-    }
-  }
-
-  // Kernels without the shared-memory aux prefetch below (large PSFs, 3-D volumes): ask
-  // L2 for the rows the epilogue will read (aux_in and the earlier chunks' partial sums)
-  // now, so they are on chip when the tap loop ends instead of costing a DRAM round trip.
-  if constexpr (NDC_L2_PREFETCH && !EDGE) {
-    const bool aux = g.final_chunk && mode_reads_aux_rt(g.mode) && !(KX <= NDC_PREFETCH_KX && g.aux_prefetch);
-    const int ox0 = tx0 + wx * kRX;
-    if ((aux || g.accum) && ox0 < g.out_ex) {
-      const long long obase = static_cast<long long>(b) * g.out_image +
-                              static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
-#pragma unroll
-      for (int j = 0; j < RY; ++j) {
-        const int row = ty0 + wy * (32 * RY) + 32 * j + lane;
-        if (row < g.out_ey) {
-          const long long o = obase + static_cast<long long>(row) * g.out_pitch;
-          if (aux) prefetch_l2(a.aux_in + o);
-          if (g.accum) prefetch_l2(a.accum_in + o);
-        }
-      }
     }
   }
 

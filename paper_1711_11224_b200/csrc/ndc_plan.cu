@@ -124,14 +124,7 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     // small PSFs are HBM-bound: 64-row tiles at 4 CTAs / SM keep more loads in flight
     if (KX_ <= kSmallMaxKX) ry_ = 1;
   }
-  if (const char* e = std::getenv("NDC_TUNE_RY")) {  // tuning hook
-    const int v = std::atoi(e);
-    if (v == 1) ry_ = 1;
-    if (v == 2 && 2 * kTileY + KY_ - 1 <= kMaxRows) ry_ = 2;
-  }
   kcy_ = std::min(KY_, kMaxRows - kTileY * ry_ + 1);  // staged rows 64*ry + kcy - 1 <= TMA box limit
-
-  if (const char* e = std::getenv("NDC_TUNE_STAGES")) stages_ = std::max(1, std::min(kMaxStages, std::atoi(e)));
 
   h64_.assign(h, h + count);
   set_taps(1.0);
@@ -164,15 +157,11 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     xlo_ = 0;
     xhi_ = mz_;
   }
-  // c0: >= 2p_x and a multiple of NDC_X_ALIGN floats (default 32 = one 128-byte line), so
-  // x-shaped output tiles cover whole lines and share none with their neighbours (a
-  // line written partly by two CTAs at different times costs DRAM read-modify-writes:
-  // measured ~2x write traffic on small PSFs at 16-byte alignment)
-  {
-    long long al = 32;
-    if (const char* e = std::getenv("NDC_X_ALIGN")) al = std::max(4LL, std::atoll(e) / 4 * 4);
-    X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, al) * al));
-  }
+  // c0: >= 2p_x and a multiple of 32 floats (one 128-byte line), so x-shaped output tiles
+  // cover whole lines and share none with their neighbours (a line written partly by two
+  // CTAs at different times costs DRAM read-modify-writes: measured ~2x write traffic on
+  // small PSFs at 16-byte alignment)
+  X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, 32) * 32));
   Y_ = Vol::make(rhi_ - rlo_, my_ + 2 * py_, mx_ + 2 * px_);
 
   int ndev = 0;
@@ -853,38 +842,12 @@ void Plan::h2d_f64_as_f32(float* dev, const double* host, size_t n) {
   }
 }
 
-// f32 device -> f64 host: the DMA of chunk i+1 overlaps the host conversion of chunk i.
-void Plan::d2h_f32_as_f64(double* host, const float* dev, size_t n) {
-  ensure_pinned();
-  const size_t chunk = kPinChunk / 4;
-  const size_t nch = (n + chunk - 1) / chunk;
-  auto issue = [&](size_t i) {
-    const int s = static_cast<int>(i & 1);
-    const size_t off = i * chunk, m = std::min(chunk, n - off);
-    check_cuda(cudaMemcpyAsync(hpin_[s], dev + off, m * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
-    check_cuda(cudaEventRecord(pin_ev_[s], stream_), "cudaEventRecord");
-  };
-  if (nch == 0) return;
-  issue(0);
-  for (size_t i = 0; i < nch; ++i) {
-    if (i + 1 < nch) issue(i + 1);
-    const int s = static_cast<int>(i & 1);
-    check_cuda(cudaEventSynchronize(pin_ev_[s]), "cudaEventSynchronize");
-    const size_t off = i * chunk, m = std::min(chunk, n - off);
-    par_convert(host + off, static_cast<const float*>(hpin_[s]), m);
-  }
-}
-
 void Plan::pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz) {
   drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
   // f64 -> f32 on the host threads, then f32 over PCIe (measured 13.8 vs 15.7 ms for the
   // config-2 batch against the f64 DMA + device conversion)
-  static const bool hostconv = [] {
-    const char* e = std::getenv("NDC_H2D_HOSTCONV");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  const bool big = hostconv && per * 8 >= (size_t(4) << 20);
+  const bool big = per * 8 >= (size_t(4) << 20);
   for (size_t b = 0; b < B_; ++b) {
     if (big) {
       h2d_f64_as_f32(static_cast<float*>(staging_), host + b * per, per);
@@ -921,28 +884,15 @@ void Plan::pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off
 void Plan::unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz) {
   drain_halos();
   const size_t per = static_cast<size_t>(nz) * v.ey * v.ex;
-  // Host-side f32 -> f64 conversion halves the PCIe bytes but measured slower than the
-  // device conversion + f64 DMA + parallel memcpy (31 vs 19 ms for 16 x 2048^2 on the
-  // 16-core box: the host conversion is bound by host memory bandwidth); off by default.
-  static const bool hostconv = [] {
-    const char* e = std::getenv("NDC_D2H_HOSTCONV");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  const bool big = hostconv && per * 8 >= (size_t(4) << 20);
+  // Device-side f32 -> f64 conversion + f64 DMA + parallel memcpy out of the pinned ring:
+  // measured faster than converting on the host (19 vs 31 ms for 16 x 2048^2 on the
+  // 16-core box: the host conversion is bound by host memory bandwidth).
   for (size_t b = 0; b < B_; ++b) {
-    if (big) {
-      check_cuda(launch_unpack_f32(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
-                                   static_cast<float*>(staging_), 1, v.geo(nz), stream_),
-                 "unpack");
-      st_[2].launches++;
-      d2h_f32_as_f64(host + b * per, static_cast<const float*>(staging_), per);
-    } else {
-      check_cuda(launch_unpack_f64(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
-                                   static_cast<double*>(staging_), 1, v.geo(nz), stream_),
-                 "unpack");
-      st_[2].launches++;
-      d2h_staged(host + b * per, staging_, per * 8);
-    }
+    check_cuda(launch_unpack_f64(dev + b * v.image + v.origin + static_cast<long long>(z_off) * v.plane,
+                                 static_cast<double*>(staging_), 1, v.geo(nz), stream_),
+               "unpack");
+    st_[2].launches++;
+    d2h_staged(host + b * per, staging_, per * 8);
   }
 }
 

@@ -59,6 +59,7 @@ LocalGroup* new_local_group(int world);
 void delete_local_group(LocalGroup* g);
 std::unique_ptr<Transport> make_local_transport(LocalGroup* g, int rank);
 void nccl_unique_id(unsigned char out[128]);
+double probe_fp32_peak(int device);  // measured FP32 FMA TFLOP/s (ndc_probe.cu)
 
 struct KernelStats {
   uint64_t launches = 0;
@@ -161,7 +162,6 @@ class Plan {
   void upload_active(const std::vector<int>& act);
   void upload_steps(const std::vector<double>& steps);
   void h2d_f64_as_f32(float* dev, const double* host, size_t n);
-  void d2h_f32_as_f64(double* host, const float* dev, size_t n);
   void pack_dense_f64(const double* host, float* dev, const Vol& v, int z_off, int nz);
   void pack_dense_f32(const float* host, float* dev, const Vol& v, int z_off, int nz);
   void unpack_dense_f64(const float* dev, double* host, const Vol& v, int z_off, int nz);

@@ -424,7 +424,40 @@ def slab_range(mz: int, pz: int, rank: int, world: int):
     return tuple(t.value for t in v)
 
 
+def probe_fp32_peak(device: int = 0) -> float:
+    """Measured FP32 FMA throughput of the device, TFLOP/s (ndc_probe_fp32_peak)."""
+    v = C.c_double()
+    _check(N.lib().ndc_probe_fp32_peak(int(device), C.byref(v)))
+    return v.value
+
+
+def _nccl_preload() -> None:
+    """Load the NCCL that torch.distributed uses (the nvidia-nccl wheel) before the library
+    opens libnccl.so.2: one libnccl.so.2 per process (shared by soname), so the plan's
+    communicator and the plumbing's must be the same build.  No-op without the wheel."""
+    global _NCCL_PRELOADED
+    if _NCCL_PRELOADED:
+        return
+    _NCCL_PRELOADED = True
+    import importlib.util
+    import os
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for d in (spec.submodule_search_locations if spec else []) or []:
+        path = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            C.CDLL(path, mode=getattr(os, "RTLD_LOCAL", 0) | getattr(os, "RTLD_NOW", 2))
+            os.environ.setdefault("NDC_NCCL_LIBRARY", path)
+            return
+
+
+_NCCL_PRELOADED = False
+
+
 def nccl_unique_id() -> bytes:
+    _nccl_preload()
     buf = C.create_string_buffer(128)
     _check(N.lib().ndc_nccl_unique_id(buf))
     return buf.raw
@@ -452,6 +485,7 @@ class Plan:
     @classmethod
     def sharded(cls, x_shape, h, rank: int, world: int, nccl_id: bytes, device: int = 0):
         h = _kernel(h)
+        _nccl_preload()
         handle = C.c_void_p()
         _check(N.lib().ndc_plan_create_sharded(C.byref(handle), int(device), h.ndim, _ext(x_shape),
                                                _ext(h.shape), _p(h), int(rank), int(world), nccl_id))
