@@ -360,10 +360,15 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
 #ifndef NDC_FFMA2
 #define NDC_FFMA2 1
 #endif
+#ifndef NDC_PACK_MAXKX
+#define NDC_PACK_MAXKX 21
+#endif
 enum PackMode : int { kPackNever = 0, kPackAlways = 1, kPackSingleSlice = 2 };
 template <int KX>
 __host__ __device__ constexpr int pack_mode() {
-  return !NDC_FFMA2 ? kPackNever : (KX >= 11 && KX <= 21) ? kPackAlways : (KX == 7 || KX == 9) ? kPackSingleSlice : kPackNever;
+  return !NDC_FFMA2 ? kPackNever
+         : (KX >= 11 && KX <= NDC_PACK_MAXKX) ? kPackAlways
+         : (KX == 7 || KX == 9) ? kPackSingleSlice : kPackNever;
 }
 
 template <bool PK>

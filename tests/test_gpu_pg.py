@@ -43,6 +43,15 @@ def _trace_close(a, b, tol, scale0=None, floor=1e-6, abs_everywhere=False):
     return bool(np.all(np.where(head, ok_head, ok_tail)))
 
 
+def _log(name, **kw):
+    path = os.environ.get("NDC_PARITY_LOG")
+    if path:
+        import json
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": name, **{k: (v if isinstance(v, (str, int)) else float(v))
+                                                 for k, v in kw.items()}}) + "\n")
+
+
 def _check(nd, d, i, tol=TOL_ITER, step=None, trace_tol=TOL_ITER):
     cfg = _cfg(nd, d[f"pg_cfg{i}"])
     if step is not None:
@@ -50,6 +59,11 @@ def _check(nd, d, i, tol=TOL_ITER, step=None, trace_tol=TOL_ITER):
     rep = nd.deconv_pg(d[f"pg_y{i}"], d[f"pg_h{i}"], tuple(int(v) for v in d[f"pg_xs{i}"]), cfg)
     ref_x, ref_obj, ref_kkt = d[f"pg_x{i}"], d[f"pg_obj{i}"], d[f"pg_kkt{i}"]
     ref_stop, ref_it = str(d[f"pg_stop{i}"]), int(d[f"pg_it{i}"])
+    n = min(len(rep.objective_trace), len(ref_obj))
+    _log(f"golden_pg{i}", estimate_rel_l2=rel_l2(rep.estimate, ref_x),
+         estimate_max_abs=float(np.max(np.abs(rep.estimate - ref_x))),
+         obj_max_rel=float(np.max(np.abs(rep.objective_trace[:n] - ref_obj[:n]) / np.maximum(np.abs(ref_obj[:n]), 1e-300))),
+         iters=int(rep.iterations_run), ref_iters=ref_it, stop=rep.stop_reason, ref_stop=ref_stop)
     assert rel_l2(rep.estimate, ref_x) <= tol or np.max(np.abs(rep.estimate - ref_x)) <= 1e-6, i
     assert np.all(rep.estimate >= 0)
     assert np.all(np.diff(rep.objective_trace) < 0)
@@ -100,29 +114,50 @@ def test_random_family(nd, golden_solvers, oracle_c):
         s_ref = oracle_c.estimate_step(d[f"pg_h{i}"], xs, 30)
         assert abs(nd.estimate_step(d[f"pg_h{i}"], xs, 30) - s_ref) <= 1e-12 * s_ref, i
         # The reference's own test asserts strict decrease, nonnegativity and trace
-        # lengths (test_solvers.cpp:95-112); these random kernels (taps in [-1, 1]) are
-        # ill-conditioned enough that float32 and f64 runs whose backtracking decisions
-        # part ways settle up to ~1e-4 apart on a flat optimum, so the estimate is held
-        # to 1e-3 here (the well-conditioned PSF cases below hold 1e-4).
-        _check(nd, d, i, tol=1e-3)
+        # lengths (test_solvers.cpp:95-112); the estimate is held to the north_star 1e-4
+        # (the f64 reference itself moves by <= 1e-7 under float32-level perturbations of
+        # its inputs on every case of this family: test_oracle.py::test_f64_sensitivity)
+        _check(nd, d, i)
 
 
-def test_acceptance6_backtracking(nd, golden_solvers):
+def test_acceptance6_backtracking(nd, golden_solvers, oracle_c):
     """acceptance.cpp:171-206: 32x32 sparse target, 5x5 sigma-1 PSF, step 8 (forces
     backtracking in ~40% of the 500 iterations).  With an 8x step the projected update
-    is only marginally contractive, so float32 rounding in the iterates is amplified:
-    the device and f64 objective traces agree to 1e-5 for the first ~25 iterations and
-    then follow different (both strictly decreasing) trajectories to the same optimum.
-    Held to: the final estimate (1e-4 relative L2, measured ~4e-7), the first 25 trace
-    entries, the iteration count / stop reason, and the acceptance criterion itself."""
+    is only marginally contractive: the f64 reference itself, rerun on inputs perturbed
+    by float32 rounding (relative 2^-24 per entry, 8 seeds), follows trajectories whose
+    objectives differ from the unperturbed run by up to ~10-70 % late in the run (they
+    meet again at the same optimum).  Held to, over ALL 500 entries of both traces: the
+    envelope of those float32-perturbed f64 runs (x2 margin, running max over a
+    +-10-iteration window); the first 25 entries to 1e-5; the final estimate to 1e-4
+    relative L2; iteration count / stop reason; the acceptance criterion itself."""
     d = golden_solvers
     i = int(d["npg"]) - 2
-    rep = nd.deconv_pg(d[f"pg_y{i}"], d[f"pg_h{i}"], (32, 32),
-                       nd.DeconvConfig(max_iters=500, tol_rel_objective=0.0, initial_step=8.0))
+    y, h = d[f"pg_y{i}"], d[f"pg_h{i}"]
+    rep = nd.deconv_pg(y, h, (32, 32), nd.DeconvConfig(max_iters=500, tol_rel_objective=0.0, initial_step=8.0))
     assert rel_l2(rep.estimate, d[f"pg_x{i}"]) <= TOL_ITER
     assert rep.iterations_run == int(d[f"pg_it{i}"]) == 500 and rep.stop_reason == "max_iters"
-    ref = d[f"pg_obj{i}"]
+    ref, kref = d[f"pg_obj{i}"], d[f"pg_kkt{i}"]
     assert np.all(np.abs(rep.objective_trace[:25] - ref[:25]) <= 1e-5 * ref[:25])
+    g = np.random.Generator(np.random.PCG64(6))
+    env_o, env_k = np.zeros(len(ref)), np.zeros(len(kref))
+    for _ in range(8):
+        yp = y * (1 + g.uniform(-1, 1, y.shape) * 2.0 ** -24)
+        hp = h * (1 + g.uniform(-1, 1, h.shape) * 2.0 ** -24)
+        r = oracle_c.deconv_pg(yp, hp, (32, 32), max_iters=500, tol_rel_objective=0.0, initial_step=8.0)
+        env_o = np.maximum(env_o, np.abs(r.objective_trace - ref))
+        env_k = np.maximum(env_k, np.abs(r.kkt_trace - kref))
+
+    def widen(e, w=10):
+        return np.array([e[max(0, k - w):k + w + 1].max() for k in range(len(e))])
+
+    dev_o = np.abs(rep.objective_trace - ref)
+    dev_k = np.abs(rep.kkt_trace - kref)
+    bound_o = 2.0 * widen(env_o) + 1e-5 * np.abs(ref)
+    bound_k = 2.0 * widen(env_k) + 1e-5 * abs(float(kref[0]))
+    _log("acceptance6", obj_dev_over_envelope=float(np.max(dev_o / bound_o)),
+         kkt_dev_over_envelope=float(np.max(dev_k / bound_k)), estimate_rel_l2=rel_l2(rep.estimate, d[f"pg_x{i}"]))
+    assert np.all(dev_o <= bound_o), int(np.argmax(dev_o / bound_o))
+    assert np.all(dev_k <= bound_k), int(np.argmax(dev_k / bound_k))
     assert np.all(np.diff(rep.objective_trace) < 0) and np.all(rep.estimate >= 0)
     assert rep.extra["backtracks"] > 100
     rel_res = np.sqrt(2 * rep.objective_trace[-1]) / np.linalg.norm(d[f"pg_y{i}"])

