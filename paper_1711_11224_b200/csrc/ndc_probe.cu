@@ -21,9 +21,9 @@ struct ProbeTaps {
 // bank (uniform datapath), a register window pair and an accumulator pair; 16 chains.
 __global__ void __launch_bounds__(256) ffma2_probe(const __grid_constant__ ProbeTaps taps, const float* in,
                                                    float* out, int iters) {
-  float win[48];
+  float2 win[24];  // register pairs (aligned: every FFMA2 operand is one 64-bit register pair)
 #pragma unroll
-  for (int i = 0; i < 48; ++i) win[i] = in[(threadIdx.x + i) & 1023];
+  for (int i = 0; i < 24; ++i) win[i] = make_float2(in[(threadIdx.x + 2 * i) & 1023], in[(threadIdx.x + 2 * i + 1) & 1023]);
   float2 acc[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) acc[c] = make_float2(0.f, 0.f);
@@ -33,10 +33,10 @@ __global__ void __launch_bounds__(256) ffma2_probe(const __grid_constant__ Probe
     for (int kp = 0; kp < 16; ++kp) {
       const float2 t = *reinterpret_cast<const float2*>(w + 2 * kp);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = __ffma2_rn(t, make_float2(win[c + 2 * kp], win[c + 2 * kp + 1]), acc[c]);
+      for (int c = 0; c < 16; ++c) acc[c] = __ffma2_rn(t, win[(c + kp) % 24], acc[c]);
     }
-    win[0] += 1.0f;
-    win[47] -= 0.5f;
+    win[0].x += 1.0f;
+    win[23].y -= 0.5f;
   }
   float s = 0.0f;
 #pragma unroll

@@ -243,3 +243,36 @@ def test_packed_ffma2_widths(nd, oracle_c, xs, hs):
     want = oracle_c.deconv_pg(yo, h, xs, max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
     assert got.iterations_run == want.iterations_run
     assert rel_l2(got.estimate, want.estimate) <= 1e-4
+
+
+@pytest.mark.parametrize("xs,hs", [((12, 40, 50), (9, 33, 33)), ((40, 37, 45), (31, 31, 31)),
+                                   ((70, 20, 36), (65, 33, 33)), ((30, 64, 70), (101, 21, 21)),
+                                   ((20, 30, 30), (41, 25, 27)), ((16, 20, 70), (47, 19, 13))])
+def test_deep_psfs_z_chunks(nd, xs, hs):
+    """3-D PSFs with more z-slices than one kernel-parameter tap block holds (config 5's
+    65x33x33 and others: 2..16 z-chunk launches accumulated through the scratch volume,
+    packed and scalar widths, edge tiles, out-of-range planes skipped): forward and adjoint
+    against the float64 oracle over the whole tensor (rel-L2; a float32 sum of up to
+    70,785 positive terms is only good to ~sqrt(K) ulp per element), and a short PG run."""
+    from oracle.oracle import Oracle
+    import os
+    fast = Oracle("fast")
+    fast.set_threads(os.cpu_count() or 1)
+    rng = np.random.default_rng(sum(xs) * 3 + sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    y_ref = fast.conv_full(x, h)
+    y = nd.conv_full(x, h)
+    assert rel_l2(y, y_ref) <= TOL_CONV
+    r = rng.uniform(-1, 1, y_ref.shape)
+    a_ref = fast.adjoint_apply(r, h, xs)
+    a = nd.adjoint_apply(r, h, xs)
+    assert rel_l2(a, a_ref) <= TOL_CONV
+    yo = y_ref + rng.uniform(0, 1e-3, y_ref.shape)
+    cfg = nd.DeconvConfig(max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    got = nd.deconv_pg(yo, h, xs, cfg)
+    want = fast.deconv_pg(yo, h, xs, max_iters=4, tol_rel_objective=0.0, initial_step=1.0)
+    assert got.iterations_run == want.iterations_run
+    assert rel_l2(got.estimate, want.estimate) <= 1e-4
+    np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)

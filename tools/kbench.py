@@ -15,7 +15,8 @@ ap.add_argument("configs", nargs="*", default=["c2"])
 ap.add_argument("--reps", type=int, default=10)
 a = ap.parse_args()
 SHAPES = {"c2": (16, (2048, 2048)), "c3": (1, (128, 256, 256)), "c4": (1, (512, 1024, 1024)),
-          "c4s": (1, (64, 1024, 1024)), "c5s": (1, (16, 2048, 2048)), "c1": (1, (256, 256)),
+          "c4s": (1, (64, 1024, 1024)), "c5s": (1, (16, 2048, 2048)),
+          "c5": (1, (256, 2048, 2048)), "c5m": (1, (64, 2048, 2048)), "c1": (1, (256, 256)),
           "c2k1": (16, (2048, 2048)), "c2k3": (16, (2048, 2048)), "c2k5": (16, (2048, 2048)),
           "c2k9": (16, (2048, 2048)), "c2k11": (16, (2048, 2048)), "c2k13": (16, (2048, 2048)),
           "c2k15": (16, (2048, 2048)), "c2k17": (16, (2048, 2048)), "c2k21": (16, (2048, 2048)),

@@ -4,7 +4,7 @@
 // taps, FFMA R, R, R) -- the latter lets one launch carry any number of z-slices.
 #include <cstdio>
 #include <cuda_runtime.h>
-constexpr int KX = 33, KXP = 36, KY = 33, P = 101, ROWS = 96;
+constexpr int KX = 33, KXP = 36, KY = 33, P = 100, ROWS = 96;
 struct Taps { float t[KY * 34]; };
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k(const __grid_constant__ Taps taps, const float* in, float* out,
