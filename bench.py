@@ -392,18 +392,25 @@ def run_ours(a):
         peak_meas = None
     peak = peak_meas or peak_theory
     if a.config in HBM_BOUND:
-        # algorithmic bytes per pass (float32): forward reads x and Y, writes r; adjoint
-        # reads r and x, writes trial and g (Plan PG passes)
-        ny_rank = B * int(np.prod([s + k - 1 for s, k in zip(x_shape, h.shape)]))
-        bytes_pass = 4.0 * ((ny_rank + 3 * vox_rank) if dom == "adjoint" else (vox_rank + 2 * ny_rank))
         hbm_peak = measured_hbm_peak()
-    traffic = None
+    # DRAM bytes of the dominant pass from the ncu capture at HEAD (tools/ncu_traffic.py:
+    # dram__bytes_read.sum + dram__bytes_write.sum over every launch of one pass, whole
+    # volume / batch on one GPU); a z-slab rank's share scales with its planes
+    traffic, traffic_basis = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(a.config, {}).get(dom)
+            t = json.load(open(tf)).get(a.config, {})
+            if t.get(dom):
+                traffic = float(t[dom]) * (vox_rank / (B * int(np.prod(x_shape))) if sharded else 1.0)
+                traffic_basis = t.get("source", "") + (" (scaled to this rank's planes)" if sharded else "")
         except (OSError, ValueError):
             traffic = None
+    # algorithmic bytes of the pass (float32): forward reads x and Y, writes r; adjoint
+    # reads r and x, writes trial and g (this rank's planes)
+    y_plane = int(np.prod([s + k - 1 for s, k in zip(x_shape[1:], h.shape[1:])]))
+    ny_rank = B * y_plane * ((yb - ya) if volume else (x_shape[0] + h.shape[0] - 1))
+    alg_bytes = 4.0 * ((ny_rank + 3 * vox_rank) if dom == "adjoint" else (vox_rank + 2 * ny_rank))
     par = "single" if world == 1 else (f"z-slab{world}" if sharded else f"replicas{world}")
     line = {
         "metric": "voxel-iterations/sec (fwd+adjoint conv) and % of FP32/HBM roofline @1/2/4/8 B200",
@@ -420,9 +427,10 @@ def run_ours(a):
                    "step_size": "auto (power iteration, untimed setup)" if work["step"] is None
                    else f"initial_step={work['step']} (unit-sum PSF)",
                    "input_generation_s": round(t_gen, 2)},
-        "roofline": ({"bound": "hbm", "kernel": dom, "achieved": bytes_pass / avg_s / 1e9, "peak": hbm_peak[0],
-                      "unit": "GB/s", "frac": bytes_pass / avg_s / 1e9 / hbm_peak[0], "traffic": traffic,
-                      "peak_basis": hbm_peak[1], "algorithmic_bytes_per_pass": bytes_pass,
+        "roofline": ({"bound": "hbm", "kernel": dom, "achieved": alg_bytes / avg_s / 1e9, "peak": hbm_peak[0],
+                      "unit": "GB/s", "frac": alg_bytes / avg_s / 1e9 / hbm_peak[0], "traffic": traffic,
+                      "traffic_basis": traffic_basis,
+                      "peak_basis": hbm_peak[1], "algorithmic_bytes_per_pass": alg_bytes,
                       "pass_ms": avg_s * 1e3, "launches_per_pass": n_dom / max(passes, 1),
                       "fp32_tflops": achieved,
                       "forward": {"launches": n_fwd, "ms": ms_fwd}, "adjoint": {"launches": n_adj, "ms": ms_adj}}
@@ -434,6 +442,7 @@ def run_ours(a):
                                     "FP32 figure" if peak_meas else
                                     f"{N_SM} SMs x 128 FFMA x 2 x {smax:.0f} MHz (probe unavailable)"),
                      "peak_theoretical": peak_theory, "frac_theoretical": achieved / peak_theory,
+                     "traffic_basis": traffic_basis, "algorithmic_bytes_per_pass": alg_bytes,
                      "algorithmic_flops_per_pass": flops_pass, "pass_ms": avg_s * 1e3,
                      "launches_per_pass": n_dom / max(passes, 1),
                      "frac_at_observed_clock": (achieved / (N_SM * FFMA_PER_SM_CLK * 2 * clk["sm_mhz"] * 1e6 / 1e12)

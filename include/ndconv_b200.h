@@ -248,6 +248,15 @@ ndc_status ndc_plan_stream(ndc_plan* plan, void** cuda_stream);
 /* Measured FP32 FMA throughput of `device` in TFLOP/s (best of 4 runs of a register-only
  * packed-FMA kernel on every SM): the roofline denominator the bench reports against. */
 ndc_status ndc_probe_fp32_peak(int device, double* tflops);
+/* Guard-band debugging (environment NDC_GUARD_BANDS=1 when the process starts): every plan
+ * allocation carries 1 MB fill-pattern guards on both sides, checked here (bad_bytes =
+ * changed guard bytes of this plan's live allocations) and when a plan is destroyed
+ * (accumulated process-wide into *total_bad by ndc_debug_guard_violations). */
+ndc_status ndc_plan_check_guards(ndc_plan* plan, size_t* bad_bytes);
+ndc_status ndc_debug_guard_violations(unsigned long long* total_bad);
+/* The checker's own test: writes 16 bytes into the guard after the plan's observation
+ * buffer (guard-band mode only; NDC_ERR_ARGUMENT otherwise). */
+ndc_status ndc_plan_debug_corrupt_guard(ndc_plan* plan);
 
 /* ---- z-slab sharding across processes (one GPU per rank, NCCL over NVLink) ----
  * Rank r of `world` owns x planes [a_r, b_r) of the slowest axis (ndc_slab_range)

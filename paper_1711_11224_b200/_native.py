@@ -89,6 +89,9 @@ _SIGS = [
     ("ndc_plan_pg_run", C.c_int, [C.c_void_p, C.POINTER(DeconvConfig)]),
     ("ndc_plan_rl_run", C.c_int, [C.c_void_p, C.POINTER(RlConfig)]),
     ("ndc_probe_fp32_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    ("ndc_plan_check_guards", C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    ("ndc_debug_guard_violations", C.c_int, [C.POINTER(C.c_ulonglong)]),
+    ("ndc_plan_debug_corrupt_guard", C.c_int, [C.c_void_p]),
     ("ndc_plan_get_report", C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(Report), dbl_p, dbl_p,
                                       C.c_size_t]),
     ("ndc_plan_get_estimate_f64", C.c_int, [C.c_void_p, dbl_p]),

@@ -600,6 +600,17 @@ ndc_status ndc_plan_create_sharded(ndc_plan** plan, int device, int ndim, const 
   });
 }
 
+ndc_status ndc_plan_check_guards(ndc_plan* plan, size_t* bad_bytes) {
+  NDC_PLAN(need(bad_bytes, "bad_bytes"); *bad_bytes = plan->p->check_guards());
+}
+ndc_status ndc_plan_debug_corrupt_guard(ndc_plan* plan) { NDC_PLAN(plan->p->debug_corrupt_guard()); }
+ndc_status ndc_debug_guard_violations(unsigned long long* total_bad) {
+  return guard([&] {
+    need(total_bad, "total_bad");
+    *total_bad = ndc::guard_violations();
+  });
+}
+
 ndc_status ndc_probe_fp32_peak(int device, double* tflops) {
   return guard([&] {
     need(tflops, "tflops");

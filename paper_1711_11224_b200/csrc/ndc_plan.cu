@@ -2,6 +2,7 @@
 // driver that restates ndconv::deconv_pg (solvers.hpp:155-238) with device-resident
 // tensors.  See ndc_plan.h for the contract and DESIGN.md for the data layout.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -39,6 +40,23 @@ double now_s() {
 }
 
 long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+}  // namespace
+
+// Guard-band mode (NDC_GUARD_BANDS=1; tests/test_gpu_guards.py): every plan allocation
+// gets kGuard bytes of a fill pattern on both sides, checked when the plan checks or
+// frees it -- an out-of-bounds device write into a neighbour's memory shows up as a
+// changed guard byte (compute-sanitizer is not available on the GPU pool).
+namespace {
+constexpr size_t kGuard = size_t(1) << 20;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("NDC_GUARD_BANDS");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+std::atomic<unsigned long long> g_guard_violations{0};
 }  // namespace
 
 void fail(int code, const std::string& msg) { throw Error{code, msg}; }
@@ -196,6 +214,12 @@ Plan::~Plan() {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  if (guard_mode()) {
+    try {
+      check_guards();
+    } catch (...) {
+    }
+  }
   for (void* p : {static_cast<void*>(x_), static_cast<void*>(trial_), static_cast<void*>(g_),
                   static_cast<void*>(trial2_), static_cast<void*>(g2_),
                   static_cast<void*>(yobs_), static_cast<void*>(r_), static_cast<void*>(rt_),
@@ -203,7 +227,7 @@ Plan::~Plan() {
                   static_cast<void*>(dsc_), static_cast<void*>(dscale_),
                   static_cast<void*>(dactive_), static_cast<void*>(dstep_), static_cast<void*>(gather_),
                   staging_})
-    if (p) cudaFreeAsync(p, stream_);
+    dfree(p);
   if (stream_) cudaStreamSynchronize(stream_);
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
   for (auto& e : halo_ev_)
@@ -223,6 +247,44 @@ Plan::~Plan() {
 // Device memory comes from the device's stream-ordered pool with the release threshold
 // raised, so destroying and re-creating plans (every one-shot C-ABI call) reuses HBM
 // instead of paying cudaMalloc / cudaFree each time.
+unsigned long long guard_violations() { return g_guard_violations.load(); }
+
+size_t Plan::check_guards() {
+  if (allocs_.empty()) return 0;
+  drain_halos();
+  check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+  if (edge_stream_) check_cuda(cudaStreamSynchronize(edge_stream_), "cudaStreamSynchronize");
+  std::vector<unsigned char> h(kGuard);
+  size_t bad = 0;
+  for (const auto& a : allocs_) {
+    for (int side = 0; side < 2; ++side) {
+      const char* src = static_cast<const char*>(a.second.first) + (side ? kGuard + a.second.second : 0);
+      check_cuda(cudaMemcpy(h.data(), src, kGuard, cudaMemcpyDeviceToHost), "D2H guard");
+      for (unsigned char c : h) bad += c != kGuardByte;
+    }
+  }
+  g_guard_violations += bad;
+  return bad;
+}
+
+// Test hook for the checker itself: overwrite 16 bytes just past the observation buffer.
+void Plan::debug_corrupt_guard() {
+  auto it = allocs_.find(yobs_);
+  if (!guard_mode() || it == allocs_.end()) fail(NDC_ERR_ARGUMENT, "guard bands are off (NDC_GUARD_BANDS=1)");
+  check_cuda(cudaMemsetAsync(static_cast<char*>(it->first) + it->second.second, 0, 16, stream_), "cudaMemset");
+}
+
+void Plan::dfree(void* p) {
+  if (p == nullptr) return;
+  auto it = allocs_.find(p);
+  if (it == allocs_.end()) {
+    cudaFreeAsync(p, stream_);
+    return;
+  }
+  cudaFreeAsync(it->second.first, stream_);
+  allocs_.erase(it);
+}
+
 void* Plan::dmalloc(size_t bytes) {
   // once per device; plans of in-process slab ranks are created from concurrent threads
   static std::once_flag pool_set[64];
@@ -236,6 +298,15 @@ void* Plan::dmalloc(size_t bytes) {
       cudaGetLastError();
     });
   void* p = nullptr;
+  if (guard_mode()) {
+    check_cuda(cudaMallocAsync(&p, bytes + 2 * kGuard, stream_), "cudaMallocAsync");
+    check_cuda(cudaMemsetAsync(p, kGuardByte, kGuard, stream_), "cudaMemset guard");
+    check_cuda(cudaMemsetAsync(static_cast<char*>(p) + kGuard + bytes, kGuardByte, kGuard, stream_),
+               "cudaMemset guard");
+    void* user = static_cast<char*>(p) + kGuard;
+    allocs_[user] = {p, bytes};
+    return user;
+  }
   check_cuda(cudaMallocAsync(&p, bytes, stream_), "cudaMallocAsync");
   return p;
 }
@@ -1266,7 +1337,7 @@ double Plan::estimate_step_f64(size_t power_iters) {
     Plan* p;
     void* q[5];
     ~Free() {
-      for (void* x : q) cudaFreeAsync(x, p->stream_);
+      for (void* x : q) p->dfree(x);
     }
   } fr{this, {dh, dhf, v, u, part}};
   check_cuda(cudaMemcpyAsync(dh, h64_.data(), K * 8, cudaMemcpyHostToDevice, stream_), "H2D");
@@ -1723,7 +1794,7 @@ void Plan::rl_run(const ndc_rl_config& c) {
     ~Restore() {
       p->drain_halos();
       p->yobs_ = y_user;
-      cudaFreeAsync(yc, p->stream_);
+      p->dfree(yc);
       p->set_taps(1.0);
     }
   } restore{this, y_user, yc};

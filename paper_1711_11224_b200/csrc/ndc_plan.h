@@ -60,6 +60,7 @@ void delete_local_group(LocalGroup* g);
 std::unique_ptr<Transport> make_local_transport(LocalGroup* g, int rank);
 void nccl_unique_id(unsigned char out[128]);
 double probe_fp32_peak(int device);  // measured FP32 FMA TFLOP/s (ndc_probe.cu)
+unsigned long long guard_violations();  // guard bytes found changed so far (process-wide)
 
 struct KernelStats {
   uint64_t launches = 0;
@@ -119,6 +120,10 @@ class Plan {
   // --- Richardson-Lucy (solvers.hpp:245-305) ---
   void rl_run(const ndc_rl_config& cfg);
 
+  // --- debugging: guard-band mode (NDC_GUARD_BANDS=1) ---
+  size_t check_guards();  // changed guard bytes around this plan's allocations (0 if off)
+  void debug_corrupt_guard();  // the checker's own test: writes 16 bytes into a guard
+
   // --- bench hooks ---
   void set_timing(bool on) { timing_ = on; }
   void reset_stats();
@@ -135,6 +140,8 @@ class Plan {
   enum Dir { kFwd = 0, kAdj = 1 };
   void alloc_all();
   void* dmalloc(size_t bytes);
+  void dfree(void* p);
+  std::map<void*, std::pair<void*, size_t>> allocs_;  // guard-band mode: user -> (base, bytes)
   float* dev_alloc_f(long long n);
   void ensure_pinned();
   void release_pinned();

@@ -431,6 +431,13 @@ def probe_fp32_peak(device: int = 0) -> float:
     return v.value
 
 
+def guard_violations() -> int:
+    """Guard bytes found changed so far in this process (NDC_GUARD_BANDS=1 only)."""
+    v = C.c_ulonglong()
+    _check(N.lib().ndc_debug_guard_violations(C.byref(v)))
+    return v.value
+
+
 def _nccl_preload() -> None:
     """Load the NCCL that torch.distributed uses (the nvidia-nccl wheel) before the library
     opens libnccl.so.2: one libnccl.so.2 per process (shared by soname), so the plan's
@@ -577,6 +584,12 @@ class Plan:
         cfg = cfg or RlConfig()
         c = N.RlConfig(int(cfg.max_iters), float(cfg.tol_rel_change))
         _check(N.lib().ndc_plan_rl_run(self.handle, C.byref(c)))
+
+    def check_guards(self) -> int:
+        """Changed guard bytes around this plan's allocations (NDC_GUARD_BANDS=1 only)."""
+        v = C.c_size_t()
+        _check(N.lib().ndc_plan_check_guards(self.handle, C.byref(v)))
+        return v.value
 
     def estimate(self, dtype=np.float64) -> np.ndarray:
         x = np.empty((self.batch,) + self.owned_x_shape(), dtype)

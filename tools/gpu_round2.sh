@@ -24,8 +24,10 @@ traffic)
 ncu)
   SHORT="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
   timeout 900 $SHORT > gpurun_out/short_$TAG.json 2>&1 && \
-  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
-      --log-file gpurun_out/launches_$TAG.csv $SHORT > gpurun_out/ncu_launch_$TAG.log 2>&1
+  # this repo's kernels only (namespace ndc::): the input generation (torch FFT / Poisson,
+  # untimed setup) is not part of the measured step
+  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled \
+      -k regex:"ndc::" -c 600 --csv --log-file gpurun_out/launches_$TAG.csv $SHORT > gpurun_out/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:correlate -s 33 -c 1 \
       -o gpurun_out/prof_c5fwd_$TAG python tools/ncu_traffic.py run c5 > gpurun_out/ncu_full_$TAG.log 2>&1
