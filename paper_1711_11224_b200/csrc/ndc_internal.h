@@ -31,6 +31,7 @@ constexpr int kMaxRows = 256;     // TMA box limit on rows: kTileY + KY - 1 <= 2
 #endif
 constexpr int kTapCap = NDC_TAP_CAP;  // taps per launch carried in the kernel parameter block
 constexpr int kMaxStages = 3;
+constexpr int kMaxDims = 8;  // tensor dimensions accepted (4+ merge into the plane axis)
 // HBM-bound small PSFs (ndc_correlate.cuh): kernel x-extents up to kStagedMaxKX use the
 // staged, sector-complete epilogue (and, for single-plane problems, a cp.async prefetch
 // of the epilogue's aux_in strip); up to kSmallMaxKX also 64-row tiles at 4 CTAs / SM.

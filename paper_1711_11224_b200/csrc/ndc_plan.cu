@@ -87,9 +87,10 @@ Vol Vol::make(int z, int y, int x, int r0, int c0) {
 Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t* k_ext,
            const double* h, std::unique_ptr<Transport> comm)
     : device_(device), B_(batch), ndim_(ndim), comm_(std::move(comm)) {
-  if (ndim < 1 || ndim > 3)
-    fail(ndim < 1 ? NDC_ERR_SHAPE : NDC_ERR_UNSUPPORTED,
-         "ndconv_b200: the device path handles 1- to 3-d tensors, got " + std::to_string(ndim));
+  if (ndim < 1) fail(NDC_ERR_SHAPE, "Shape: need at least one dimension");
+  if (ndim > kMaxDims)
+    fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: at most " + std::to_string(kMaxDims) + " dimensions, got " +
+                                  std::to_string(ndim));
   if (batch == 0) fail(NDC_ERR_ARGUMENT, "ndconv_b200: batch must be positive");
   size_t count = 1;
   for (int i = 0; i < ndim; ++i) {
@@ -100,10 +101,68 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   }
   for (size_t i = 0; i < count; ++i)
     if (!std::isfinite(h[i])) fail(NDC_ERR_NUMERIC, "Kernel: values must be finite");
-  const int lead = 3 - ndim;
-  for (int i = 0; i < ndim; ++i) {
-    xext_[lead + i] = x_ext[i];
-    kext_[lead + i] = k_ext[i];
+  uext_x_.assign(x_ext, x_ext + ndim);
+  uext_k_.assign(k_ext, k_ext + ndim);
+  std::vector<double> hm;  // the kernel on the merged plane axis (ndim > 3)
+  if (ndim <= 3) {
+    const int lead = 3 - ndim;
+    for (int i = 0; i < ndim; ++i) {
+      xext_[lead + i] = x_ext[i];
+      kext_[lead + i] = k_ext[i];
+    }
+  } else {
+    // More than 3 dimensions (the reference recurses over any ndim, convolution.hpp:55-74):
+    // dims 0 .. ndim-3 merge into ONE plane axis with the observation's strides, y
+    // plane index Z = sum_i z_i S_i (S_{L-1} = 1, S_i = S_{i+1} Y_{i+1}, Y_i = m_i + k_i - 1).
+    // x sits at the same indices (zero planes where some z_i >= m_i) and the kernel at
+    // J = sum_i j_i S_i (zero slices elsewhere), so a full / valid correlation along the
+    // merged axis is exactly the n-d one: Z = z + j never carries between dims because
+    // z_i + j_i < Y_i.  The forward pass skips the all-zero tap slices (see build_chunks),
+    // the adjoint computes only x's real planes (xruns_), so the zero planes stay zero.
+    if (batch != 1) fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: batches of tensors with more than 3 dimensions");
+    if (comm_) fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: z-slab sharding handles 1- to 3-d tensors");
+    merged_ = true;
+    const int L = ndim - 2;
+    std::vector<long long> Y(L), S(L);
+    for (int i = 0; i < L; ++i) Y[i] = static_cast<long long>(x_ext[i] + k_ext[i] - 1);
+    S[L - 1] = 1;
+    for (int i = L - 2; i >= 0; --i) S[i] = S[i + 1] * Y[i + 1];
+    const long long P = S[0] * Y[0];
+    long long KZm = 1;
+    for (int i = 0; i < L; ++i) KZm += static_cast<long long>(k_ext[i] - 1) * S[i];
+    const long long kyx = static_cast<long long>(k_ext[ndim - 2]) * k_ext[ndim - 1];
+    if (P > (1LL << 30) || KZm * kyx > (1LL << 28))
+      fail(NDC_ERR_UNSUPPORTED, "ndconv_b200: merged leading dimensions too large");
+    xext_[0] = static_cast<size_t>(P);
+    xext_[1] = x_ext[ndim - 2];
+    xext_[2] = x_ext[ndim - 1];
+    kext_[0] = static_cast<size_t>(KZm);
+    kext_[1] = k_ext[ndim - 2];
+    kext_[2] = k_ext[ndim - 1];
+    hm.assign(static_cast<size_t>(KZm * kyx), 0.0);
+    for (size_t f = 0; f < count; ++f) {
+      size_t rem = f / static_cast<size_t>(kyx);
+      long long J = 0;
+      for (int i = L - 1; i >= 0; --i) {
+        J += static_cast<long long>(rem % k_ext[i]) * S[i];
+        rem /= k_ext[i];
+      }
+      hm[static_cast<size_t>(J * kyx) + f % static_cast<size_t>(kyx)] = h[f];
+    }
+    // x's real planes: one run of m_{L-1} planes per leading index (z_0 .. z_{L-2})
+    std::vector<size_t> idx(L - 1, 0);
+    for (;;) {
+      long long start = 0;
+      for (int i = 0; i < L - 1; ++i) start += static_cast<long long>(idx[i]) * S[i];
+      xruns_.push_back({static_cast<int>(start), static_cast<int>(x_ext[L - 1])});
+      int i = L - 2;
+      for (; i >= 0; --i) {
+        if (++idx[i] < x_ext[i]) break;
+        idx[i] = 0;
+      }
+      if (i < 0) break;
+    }
+    ny_user_planes_ = static_cast<int>(P);
   }
   mz_ = static_cast<int>(xext_[0]);
   my_ = static_cast<int>(xext_[1]);
@@ -144,7 +203,10 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   }
   kcy_ = std::min(KY_, kMaxRows - kTileY * ry_ + 1);  // staged rows 64*ry + kcy - 1 <= TMA box limit
 
-  h64_.assign(h, h + count);
+  if (merged_)
+    h64_ = std::move(hm);
+  else
+    h64_.assign(h, h + count);
   set_taps(1.0);
   kernel_all_zero_ = true;
   for (size_t i = 0; i < count; ++i)
@@ -181,6 +243,12 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   // small PSFs at 16-byte alignment)
   X_ = Vol::make(xhi_ - xlo_, my_, mx_, 2 * py_, static_cast<int>(cdiv(2 * px_, 32) * 32));
   Y_ = Vol::make(rhi_ - rlo_, my_ + 2 * py_, mx_ + 2 * px_);
+  if (!merged_) {
+    xruns_.assign(1, {0, xa_n_});
+    ny_user_planes_ = yb_ - ya_;
+  }
+  nreal_x_ = 1;
+  for (size_t e : uext_x_) nreal_x_ *= static_cast<double>(e);
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -538,7 +606,7 @@ void Plan::alloc_all() {
   r_ = dev_alloc_f(ny);
   rt_ = dev_alloc_f(ny);
   // partial sums of multi-launch (chunked) PSFs, see correlate()
-  const bool chunked = KX_ > kMaxKX || KY_ > kcy_ || KZ_ > kTapCap / (KY_ * tap_pitch(KX_));
+  const bool chunked = chunks_fwd_.size() > 1 || chunks_adj_.size() > 1;
   if (chunked) scratch_ = dev_alloc_f(std::max(nx, ny));
   partials_cap_ = static_cast<long long>(B_) *
                   std::max({partials_per_image(kFwd), partials_per_image(kAdj),
@@ -631,22 +699,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   g.mode = mode;
   const int off_x0 = g.off_x, off_y0 = g.off_y;
   const int kxp_full = tap_pitch(KX_);
-  // Tap chunks: columns [kx0, kx0 + cw) (instantiation width w >= cw, zero padded), rows
-  // [ky0, ky0 + cy), z-slices [kz0, kz1).  One chunk for every PSF up to 33 columns,
-  // kcy_ rows and kTapCap taps (all BASELINE configs but config 5, which splits in z).
-  struct Chunk {
-    int kx0, cw, w, ky0, cy, kz0, kz1;
-  };
-  std::vector<Chunk> chunks;
-  for (int kx0 = 0; kx0 < KX_; kx0 += (KX_ <= kMaxKX ? KX_ : kMaxKX - 1)) {
-    const int cw = KX_ <= kMaxKX ? KX_ : std::min(kMaxKX - 1, KX_ - kx0);
-    const int w = (cw % 2) ? cw : cw + 1;
-    for (int ky0 = 0; ky0 < KY_; ky0 += kcy_) {
-      const int cy = std::min(kcy_, KY_ - ky0);
-      const int slices = std::max(1, kTapCap / (cy * tap_pitch(w)));
-      for (int kz0 = 0; kz0 < KZ_; kz0 += slices) chunks.push_back({kx0, cw, w, ky0, cy, kz0, std::min(KZ_, kz0 + slices)});
-    }
-  }
+  const std::vector<TapChunk>& chunks = fwd ? chunks_fwd_ : chunks_adj_;
   static thread_local TapBlock tb;
   // One launch per tap chunk and plane segment [z_base, z_base + nz) of the computed
   // planes.  A segment that does not start at plane 0 shifts the output / input plane
@@ -661,7 +714,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   struct Seg {
     int z_base, nz;
   };
-  auto run_chunks = [&](std::initializer_list<Seg> segs) {
+  auto run_chunks = [&](const std::vector<Seg>& segs) {
     size_t ev = 0;
     if (timing_) {
       if (ev_used_ == ev_pool_.size()) {
@@ -683,7 +736,7 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
       g.out_z0 = out_z0_base + sg.z_base;
       g.off_z = off_z_base + sg.z_base;
       for (size_t c = 0; c < chunks.size(); ++c) {
-        const Chunk& ch = chunks[c];
+        const TapChunk& ch = chunks[c];
         g.KY = ch.cy;
         g.rows = kTileY * ry_ + ch.cy - 1;
         g.pitch_s = shared_pitch_for(ch.w, sh);
@@ -750,7 +803,17 @@ void Plan::correlate(Dir d, const float* in, float* out, int mode, float* aux_ou
   const int lo = (world_ > 1 && rank_ > 0) ? pz_ : 0;
   const int hi = (world_ > 1 && rank_ + 1 < world_) ? pz_ : 0;
   const int n_int = nz_out - lo - hi;
-  if (halo_overlap_ && (lo + hi) > 0 && n_int > 0) {
+  if (merged_ && !fwd) {
+    // x-shaped outputs of a merged (ndim > 3) plan: only x's real planes; the partial
+    // slots of the skipped planes are zeroed so the per-pass reductions ignore them
+    if (partials)
+      check_cuda(cudaMemsetAsync(partials_, 0, partials_per_image(kAdj) * sizeof(double2), stream_),
+                 "cudaMemset partials");
+    std::vector<Seg> segs;
+    for (const auto& r : xruns_) segs.push_back({r.first, r.second});
+    wait_halo(in);
+    run_chunks(segs);
+  } else if (halo_overlap_ && (lo + hi) > 0 && n_int > 0) {
     run_chunks({{lo, n_int}});
     wait_halo(in);
     run_chunks({{0, lo}, {nz_out - hi, hi}});
@@ -980,29 +1043,39 @@ void Plan::unpack_dense_f32(const float* dev, float* host, const Vol& v, int z_o
 }
 
 void Plan::set_observation_f64(const double* y) {
-  pack_dense_f64(y, yobs_, Y_, ya_ - rlo_, yb_ - ya_);
+  pack_dense_f64(y, yobs_, Y_, ya_ - rlo_, ny_user_planes_);
   halo_y(yobs_);
 }
 void Plan::set_observation_f32(const float* y) {
-  pack_dense_f32(y, yobs_, Y_, ya_ - rlo_, yb_ - ya_);
+  pack_dense_f32(y, yobs_, Y_, ya_ - rlo_, ny_user_planes_);
   halo_y(yobs_);
 }
 void Plan::set_x_f64(const double* x) {
-  pack_dense_f64(x, x_, X_, xa_ - xlo_, xa_n_);
+  for (size_t r = 0; r < xruns_.size(); ++r)
+    pack_dense_f64(x + r * xrun_elems(), x_, X_, xa_ - xlo_ + xruns_[r].first, xruns_[r].second);
   halo_x(x_);
 }
 void Plan::set_x_f32(const float* x) {
-  pack_dense_f32(x, x_, X_, xa_ - xlo_, xa_n_);
+  for (size_t r = 0; r < xruns_.size(); ++r)
+    pack_dense_f32(x + r * xrun_elems(), x_, X_, xa_ - xlo_ + xruns_[r].first, xruns_[r].second);
   halo_x(x_);
 }
-void Plan::get_y_buffer_f32(float* y) { unpack_dense_f32(r_, y, Y_, ya_ - rlo_, yb_ - ya_); }
-void Plan::get_x_buffer_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
-void Plan::get_estimate_f64(double* x) { unpack_dense_f64(x_, x, X_, xa_ - xlo_, xa_n_); }
-void Plan::get_estimate_f32(float* x) { unpack_dense_f32(x_, x, X_, xa_ - xlo_, xa_n_); }
-void Plan::get_observation_f64(double* y) { unpack_dense_f64(yobs_, y, Y_, ya_ - rlo_, yb_ - ya_); }
-void Plan::get_y_buffer_f64(double* y) { unpack_dense_f64(r_, y, Y_, ya_ - rlo_, yb_ - ya_); }
+void Plan::get_y_buffer_f32(float* y) { unpack_dense_f32(r_, y, Y_, ya_ - rlo_, ny_user_planes_); }
+void Plan::get_x_buffer_f32(float* x) {
+  for (size_t r = 0; r < xruns_.size(); ++r)
+    unpack_dense_f32(x_, x + r * xrun_elems(), X_, xa_ - xlo_ + xruns_[r].first, xruns_[r].second);
+}
+void Plan::get_estimate_f64(double* x) {
+  for (size_t r = 0; r < xruns_.size(); ++r)
+    unpack_dense_f64(x_, x + r * xrun_elems(), X_, xa_ - xlo_ + xruns_[r].first, xruns_[r].second);
+}
+void Plan::get_estimate_f32(float* x) { get_x_buffer_f32(x); }
+void Plan::get_observation_f64(double* y) { unpack_dense_f64(yobs_, y, Y_, ya_ - rlo_, ny_user_planes_); }
+void Plan::get_y_buffer_f64(double* y) { unpack_dense_f64(r_, y, Y_, ya_ - rlo_, ny_user_planes_); }
 void Plan::get_x_buffer_f64(double* x, int which) {
-  unpack_dense_f64(which == 0 ? x_ : g_, x, X_, xa_ - xlo_, xa_n_);
+  for (size_t r = 0; r < xruns_.size(); ++r)
+    unpack_dense_f64(which == 0 ? x_ : g_, x + r * xrun_elems(), X_, xa_ - xlo_ + xruns_[r].first,
+                     xruns_[r].second);
 }
 
 // ---- operators ------------------------------------------------------------------------
@@ -1057,14 +1130,14 @@ void Plan::estimate_launch(size_t power_iters) {
   drain_halos();
   if (power_iters == 0) fail(NDC_ERR_CONFIG, "estimate_step: power_iters must be positive");
   if (kernel_all_zero_) fail(NDC_ERR_NUMERIC, "estimate_step: degenerate all-zero kernel");
-  const double n = static_cast<double>(mz_) * my_ * mx_;
+  const double n = nreal_x_;
   estimate_pending_ = 0;
   // Small problems run the power iteration in float64: when all-ones is an exact but
   // non-dominant eigenvector of A^T A (symmetric tiny shapes), the reference's f64
   // iteration stays in that eigenspace and float32 rounding would not.
   const char* sep_env = std::getenv("NDC_SEPARABLE_STEP");  // 0: off, 2: also small problems (tests)
   const bool sep_small = sep_env != nullptr && std::atoi(sep_env) == 2;
-  if (world_ == 1 && n * static_cast<double>(h64_.size()) <= static_cast<double>(1 << 28) &&
+  if (world_ == 1 && !merged_ && n * static_cast<double>(h64_.size()) <= static_cast<double>(1 << 28) &&
       !(sep_small && estimate_step_separable(power_iters, &estimate_value_))) {
     estimate_value_ = estimate_step_f64(power_iters);
     estimate_pending_ = power_iters;
@@ -1083,10 +1156,7 @@ void Plan::estimate_launch(size_t power_iters) {
   try {
     const float one = 1.0f;
     check_cuda(cudaMemcpyAsync(dscale_, &one, 4, cudaMemcpyHostToDevice, stream_), "H2D");
-    check_cuda(launch_fill(x_owned(g_), static_cast<float>(1.0 / std::sqrt(n)), 1, X_.geo(xa_n_),
-                           stream_),
-               "fill");
-    st_[2].launches++;
+    fill_x_real(g_, 0, static_cast<float>(1.0 / std::sqrt(n)));
     double* lam = dsc_ + kNumSlots * saveB;
     for (size_t i = 0; i < power_iters; ++i) {
       halo_x(g_);
@@ -1188,11 +1258,7 @@ size_t chunk_io(bool write, int fd, double* buf, size_t n, size_t off, bool& io_
 std::vector<size_t> Plan::user_shape(bool y) const {
   std::vector<size_t> e;
   if (B_ > 1) e.push_back(B_);
-  const int lead = 3 - ndim_;
-  for (int i = 0; i < ndim_; ++i) {
-    const size_t k = kext_[lead + i];
-    e.push_back(y ? xext_[lead + i] + k - 1 : xext_[lead + i]);
-  }
+  for (int i = 0; i < ndim_; ++i) e.push_back(y ? uext_x_[i] + uext_k_[i] - 1 : uext_x_[i]);
   return e;
 }
 
@@ -1207,8 +1273,8 @@ void Plan::load_observation_ndtensor(const std::string& path) {
   Fd fd{::open(path.c_str(), O_RDONLY)};
   if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path);
   const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;                       // dense
-  const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;               // one image
-  const size_t own = static_cast<size_t>(yb_ - ya_) * plane;
+  const size_t full = static_cast<size_t>(y_planes_total()) * plane;            // one image
+  const size_t own = static_cast<size_t>(ny_user_planes_) * plane;
   const size_t chunk = kPinChunk / 8;
   size_t i = 0;
   for (size_t b = 0; b < B_; ++b) {
@@ -1230,7 +1296,7 @@ void Plan::load_observation_ndtensor(const std::string& path) {
     }
     check_cuda(launch_pack_f64(static_cast<const double*>(staging_),
                                yobs_ + b * Y_.image + static_cast<long long>(ya_ - rlo_) * Y_.plane, 1,
-                               Y_.geo(yb_ - ya_), stream_),
+                               Y_.geo(ny_user_planes_), stream_),
                "pack");
     st_[2].launches++;
   }
@@ -1245,7 +1311,7 @@ void Plan::save_estimate_ndtensor(const std::string& path) {
   const std::vector<size_t> ext = user_shape(false);
   const std::string hl = ndtensor_header_line(ext);
   const size_t plane = static_cast<size_t>(my_) * mx_;
-  const size_t full = static_cast<size_t>(mz_) * plane;
+  const size_t full = static_cast<size_t>(nreal_x_);  // one image (a merged plan's real voxels)
   if (rank_ == 0) {  // header + full-size file, then every rank fills its planes
     Fd fd{::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644)};
     if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
@@ -1260,14 +1326,17 @@ void Plan::save_estimate_ndtensor(const std::string& path) {
   ensure_pinned();
   Fd fd{::open(path.c_str(), O_WRONLY)};
   if (fd.fd < 0) fail(NDC_ERR_FORMAT, "cannot open " + path + " for writing");
-  const size_t own = static_cast<size_t>(xa_n_) * plane;
+  const size_t own = merged_ ? full : static_cast<size_t>(xa_n_) * plane;
   const size_t chunk = kPinChunk / 8;
   const size_t nchunks = (own + chunk - 1) / chunk;
   for (size_t b = 0; b < B_; ++b) {
-    check_cuda(launch_unpack_f64(x_owned(x_) + b * X_.image, static_cast<double*>(staging_), 1,
-                                 X_.geo(xa_n_), stream_),
-               "unpack");
-    st_[2].launches++;
+    for (size_t r = 0; r < xruns_.size(); ++r) {  // one run unless merged
+      check_cuda(launch_unpack_f64(x_owned(x_) + b * X_.image + static_cast<long long>(xruns_[r].first) * X_.plane,
+                                   static_cast<double*>(staging_) + r * xrun_elems(), 1, X_.geo(xruns_[r].second),
+                                   stream_),
+                 "unpack");
+      st_[2].launches++;
+    }
     const size_t first = b * full + static_cast<size_t>(xa_) * plane;
     auto d2h = [&](size_t k) {
       const size_t n = std::min(chunk, own - k * chunk);
@@ -1304,15 +1373,15 @@ void Plan::add_gaussian_noise(double mean, double std_dev, uint64_t seed) {
   drain_halos();
   if (std_dev < 0) fail(NDC_ERR_NUMERIC, "add_gaussian_noise: std_dev must be >= 0");
   const size_t plane = static_cast<size_t>(Y_.ey) * Y_.ex;
-  const size_t full = static_cast<size_t>(mz_ + 2 * pz_) * plane;
-  const size_t own = static_cast<size_t>(yb_ - ya_) * plane;
+  const size_t full = static_cast<size_t>(y_planes_total()) * plane;
+  const size_t own = static_cast<size_t>(ny_user_planes_) * plane;
   double* dense = static_cast<double*>(staging_);
   GaussianNoise noise(seed, mean, std_dev, stream_);
   for (size_t b = 0; b < B_; ++b) {
     float* base = yobs_ + b * Y_.image + static_cast<long long>(ya_ - rlo_) * Y_.plane;
-    check_cuda(launch_unpack_f64(base, dense, 1, Y_.geo(yb_ - ya_), stream_), "unpack");
+    check_cuda(launch_unpack_f64(base, dense, 1, Y_.geo(ny_user_planes_), stream_), "unpack");
     noise.add(dense, own, b * full + static_cast<size_t>(ya_) * plane);
-    check_cuda(launch_pack_f64(dense, base, 1, Y_.geo(yb_ - ya_), stream_), "pack");
+    check_cuda(launch_pack_f64(dense, base, 1, Y_.geo(ny_user_planes_), stream_), "pack");
     st_[2].launches += 2;
   }
   sync();
@@ -1395,6 +1464,7 @@ double Plan::collect_lambdas(size_t power_iters) {
 // to rounding (tests/test_gpu_step.py).  Small problems keep the device float64 path
 // (reference-exact on the tiny KATs); NDC_SEPARABLE_STEP=0 disables this path.
 bool Plan::estimate_step_separable(size_t power_iters, double* step) {
+  if (merged_) return false;  // the merged plane axis carries zero planes: not a Kronecker product
   if (const char* e = std::getenv("NDC_SEPARABLE_STEP"))
     if (std::atoi(e) == 0) return false;
   if (h64_.empty()) return false;
@@ -1677,6 +1747,16 @@ size_t Plan::pg_iterate(size_t n) {
   return active_count;
 }
 
+// Fill image b's real x planes (a merged plan's zero planes stay zero).
+void Plan::fill_x_real(float* buf, size_t b, float v) {
+  for (const auto& r : xruns_) {
+    check_cuda(launch_fill(x_owned(buf) + b * X_.image + static_cast<long long>(r.first) * X_.plane, v, 1,
+                           X_.geo(r.second), stream_),
+               "fill");
+    st_[2].launches++;
+  }
+}
+
 void Plan::copy_image_x(float* dst, const float* src, size_t b) {
   drain_halos();
   check_cuda(cudaMemcpyAsync(dst + b * X_.image, src + b * X_.image, X_.image * 4,
@@ -1756,6 +1836,47 @@ void Plan::set_taps(double scale) {
     taps_adj_[(i / KX_) * kxp + i % KX_] = v;
     taps_fwd_[(j / KX_) * kxp + j % KX_] = v;
   }
+  chunks_fwd_ = build_chunks(taps_fwd_);
+  chunks_adj_ = build_chunks(taps_adj_);
+}
+
+// Tap chunks of one direction: columns [kx0, kx0 + cw) (instantiation width w >= cw, zero
+// padded), rows [ky0, ky0 + cy), z-slices [kz0, kz1).  One chunk for every PSF up to 33
+// columns, kcy_ rows and kTapCap taps (all BASELINE configs but config 5, which splits
+// in z).  z-slices whose taps are all zero are skipped (they add exact zeros): the merged
+// plane axis of a tensor with more than 3 dimensions is mostly such slices.
+std::vector<TapChunk> Plan::build_chunks(const std::vector<float>& taps) const {
+  const int kxp = tap_pitch(KX_);
+  const size_t slice = static_cast<size_t>(KY_) * kxp;
+  std::vector<std::pair<int, int>> zruns;  // maximal runs of slices with a nonzero tap
+  for (int kz = 0; kz < KZ_;) {
+    const bool nz = std::any_of(taps.begin() + kz * slice, taps.begin() + (kz + 1) * slice,
+                                [](float v) { return v != 0.0f; });
+    if (!nz) {
+      ++kz;
+      continue;
+    }
+    int e = kz + 1;
+    while (e < KZ_ && std::any_of(taps.begin() + e * slice, taps.begin() + (e + 1) * slice,
+                                  [](float v) { return v != 0.0f; }))
+      ++e;
+    zruns.push_back({kz, e});
+    kz = e;
+  }
+  if (zruns.empty()) zruns.push_back({0, KZ_});  // an all-zero kernel still runs (zero output)
+  std::vector<TapChunk> chunks;
+  for (int kx0 = 0; kx0 < KX_; kx0 += (KX_ <= kMaxKX ? KX_ : kMaxKX - 1)) {
+    const int cw = KX_ <= kMaxKX ? KX_ : std::min(kMaxKX - 1, KX_ - kx0);
+    const int w = (cw % 2) ? cw : cw + 1;
+    for (int ky0 = 0; ky0 < KY_; ky0 += kcy_) {
+      const int cy = std::min(kcy_, KY_ - ky0);
+      const int slices = std::max(1, kTapCap / (cy * tap_pitch(w)));
+      for (const auto& zr : zruns)
+        for (int kz0 = zr.first; kz0 < zr.second; kz0 += slices)
+          chunks.push_back({kx0, cw, w, ky0, cy, kz0, std::min(zr.second, kz0 + slices)});
+    }
+  }
+  return chunks;
 }
 
 // Richardson-Lucy (solvers.hpp:245-305) on the same operators: the kernel normalised to
@@ -1814,7 +1935,7 @@ void Plan::rl_run(const ndc_rl_config& c) {
   halo_y(yobs_);
   std::vector<double> total(B_);
   std::vector<int> act(B_, 1);
-  const double n = static_cast<double>(mz_) * my_ * mx_;
+  const double n = nreal_x_;
   for (size_t b = 0; b < B_; ++b) {
     total[b] = hsc_[kAUX * B_ + b];
     img_[b].clamped = static_cast<size_t>(hsc_[kCHG * B_ + b]);
@@ -1822,8 +1943,7 @@ void Plan::rl_run(const ndc_rl_config& c) {
   // x0 per image: total/n, or 0 for an all-zero observation (solvers.hpp:263-270)
   for (size_t b = 0; b < B_; ++b) {
     const float v = total[b] > 0.0 ? static_cast<float>(total[b] / n) : 0.0f;
-    check_cuda(launch_fill(x_owned(x_) + b * X_.image, v, 1, X_.geo(xa_n_), stream_), "fill");
-    st_[2].launches++;
+    fill_x_real(x_, b, v);
   }
   halo_x(x_);
 

@@ -62,6 +62,11 @@ void nccl_unique_id(unsigned char out[128]);
 double probe_fp32_peak(int device);  // measured FP32 FMA TFLOP/s (ndc_probe.cu)
 unsigned long long guard_violations();  // guard bytes found changed so far (process-wide)
 
+// One launch's share of the taps (see Plan::build_chunks).
+struct TapChunk {
+  int kx0, cw, w, ky0, cy, kz0, kz1;
+};
+
 struct KernelStats {
   uint64_t launches = 0;
   double ms = 0.0;
@@ -133,8 +138,8 @@ class Plan {
   void bench_adjoint();
 
   size_t batch() const { return B_; }
-  size_t x_count() const { return static_cast<size_t>(xa_n_) * my_ * mx_; }  // owned, per image
-  size_t y_count() const { return static_cast<size_t>(yb_ - ya_) * (my_ + 2 * py_) * (mx_ + 2 * px_); }
+  size_t x_count() const { return xruns_.size() * xrun_elems(); }  // owned, per image
+  size_t y_count() const { return static_cast<size_t>(ny_user_planes_) * (my_ + 2 * py_) * (mx_ + 2 * px_); }
 
  private:
   enum Dir { kFwd = 0, kAdj = 1 };
@@ -164,6 +169,11 @@ class Plan {
   void wait_halo(const float* buf);  // plan stream waits for buf's pending exchange
   void drain_halos();                // ... for every pending exchange
   void copy_image_x(float* dst, const float* src, size_t b);
+  void fill_x_real(float* buf, size_t b, float v);
+  int y_planes_total() const { return merged_ ? ny_user_planes_ : mz_ + 2 * pz_; }  // per image
+  size_t xrun_elems() const {  // dense caller elements of one x run
+    return xruns_.empty() ? 0 : static_cast<size_t>(xruns_[0].second) * my_ * mx_;
+  }
   void copy_image_y(float* dst, const float* src, size_t b);
   void sync();
   void upload_active(const std::vector<int>& act);
@@ -181,7 +191,14 @@ class Plan {
   cudaStream_t stream_ = nullptr;
   size_t B_ = 1;
   int ndim_ = 1;
-  size_t xext_[3] = {1, 1, 1}, kext_[3] = {1, 1, 1};
+  size_t xext_[3] = {1, 1, 1}, kext_[3] = {1, 1, 1};  // the 3-d problem the kernels run
+  std::vector<size_t> uext_x_, uext_k_;              // the caller's extents (any ndim)
+  // ndim > 3: leading dims merged into the plane axis (see the constructor); x's real
+  // planes are the runs xruns_ = (first owned plane, count), the rest stay zero
+  bool merged_ = false;
+  std::vector<std::pair<int, int>> xruns_;
+  int ny_user_planes_ = 0;  // observation planes the caller passes (owned)
+  double nreal_x_ = 0;      // x voxels per image (the caller's)
   int mz_ = 1, my_ = 1, mx_ = 1;
   int KZ_ = 1, KY_ = 1, KX_ = 1, pz_ = 0, py_ = 0, px_ = 0;
   int kcx_ = 1, kcy_ = 1;  // tap-chunk extents of one launch (x <= kMaxKX, rows <= TMA box)
@@ -190,6 +207,8 @@ class Plan {
   std::vector<float> taps_fwd_, taps_adj_;
   std::vector<double> h64_;     // the kernel as given (f64, flat)
   void set_taps(double scale);  // taps = float(h * scale), forward flipped, rows padded
+  std::vector<TapChunk> build_chunks(const std::vector<float>& taps) const;
+  std::vector<TapChunk> chunks_fwd_, chunks_adj_;
   bool kernel_all_zero_ = false;
 
   // z-slab geometry (global plane indices); unsharded: one slab holding everything.

@@ -134,7 +134,7 @@ def test_error_classes(nd):
     with pytest.raises(nd.Error):
         nd.deconv_pg(np.zeros(6), [0.1, 0.8, 0.1], (4,), nd.DeconvConfig(max_iters=0))
     with pytest.raises(nd.UnsupportedError):
-        nd.conv_full(np.ones((2, 2, 2, 2)), np.ones((1, 1, 1, 1)))  # the device path is 1- to 3-d
+        nd.conv_full(np.ones((1,) * 9), np.ones((1,) * 9))  # at most 8 dimensions
 
 
 @pytest.mark.parametrize("xs,hs", [((37, 50), (3, 35)), ((60, 90), (37, 71)), ((50, 40), (201, 3)),
@@ -276,3 +276,47 @@ def test_deep_psfs_z_chunks(nd, xs, hs):
     assert got.iterations_run == want.iterations_run
     assert rel_l2(got.estimate, want.estimate) <= 1e-4
     np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
+
+
+ND_CASES = [((3, 4, 10, 12), (3, 1, 3, 5)), ((2, 3, 2, 8, 9), (1, 3, 3, 3, 5)), ((2, 3, 6, 7), (5, 3, 3, 3)),
+            ((2, 2, 2, 2, 5, 6), (3, 1, 3, 1, 3, 3)), ((4, 5, 33, 40), (3, 3, 7, 9))]
+
+
+@pytest.mark.parametrize("xs,hs", ND_CASES)
+def test_more_than_three_dims(nd, xs, hs):
+    """Tensors with 4-6 dimensions (the reference recurses over any ndim,
+    convolution.hpp:55-74): the leading dimensions merge into the plane axis with the
+    observation's strides (zero planes / zero tap slices in between).  Against the
+    reference compiled from its sources (oracle/_ref; the C restatement where it is not
+    built): every element of forward and adjoint, a PG run with backtracking, and the
+    step estimate."""
+    from oracle.oracle import Oracle, available
+    ref = Oracle("ref" if available("ref") else "c")
+    rng = np.random.default_rng(sum(xs) + 10 * sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    y_ref = ref.conv_full(x, h)
+    y = nd.conv_full(x, h)
+    assert y.shape == y_ref.shape
+    assert np.max(np.abs(y - y_ref)) <= 1e-5 * np.max(np.abs(y_ref))
+    r = rng.uniform(-1, 1, y_ref.shape)
+    a_ref = ref.adjoint_apply(r, h, xs)
+    assert np.max(np.abs(nd.adjoint_apply(r, h, xs) - a_ref)) <= 1e-5 * np.max(np.abs(a_ref))
+    yo = y_ref + rng.uniform(0, 1e-3, y_ref.shape)
+    for step in (1.0, 8.0):
+        cfg = nd.DeconvConfig(max_iters=12, tol_rel_objective=0.0, initial_step=step)
+        got = nd.deconv_pg(yo, h, xs, cfg)
+        want = ref.deconv_pg(yo, h, xs, max_iters=12, tol_rel_objective=0.0, initial_step=step)
+        assert got.estimate.shape == tuple(xs)
+        assert got.iterations_run == want.iterations_run and got.stop_reason == want.stop_reason
+        assert rel_l2(got.estimate, want.estimate) <= 1e-4, step
+        np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
+    s_ref = ref.estimate_step(h, xs, 30)
+    assert abs(nd.estimate_step(h, xs, 30) - s_ref) <= 1e-5 * s_ref
+    # the plan keeps the caller's shapes
+    with nd.Plan(xs, h) as p:
+        p.set_observation(yo)
+        assert np.array_equal(p.observation()[0], yo.astype(np.float32).astype(np.float64))
+        p.pg_run(nd.DeconvConfig(max_iters=3, tol_rel_objective=0.0, initial_step=1.0))
+        assert p.estimate()[0].shape == tuple(xs)

@@ -237,3 +237,37 @@ def test_f64_sensitivity_of_the_golden_family(oracle_c, golden_solvers):
             hp = h * (1 + g.uniform(-1, 1, h.shape) * 2.0 ** -24)
             r = oracle_c.deconv_pg(yp, hp, xs, **_pg_kwargs(d[f"pg_cfg{i}"]))
             assert _rel(r.estimate, d[f"pg_x{i}"]) <= 1e-6, i
+
+
+@pytest.mark.skipif(not available("ref"), reason="oracle/_ref not built")
+def test_oracle_more_than_three_dims_bitwise():
+    """4-6-d tensors: the C restatement equals the compiled reference bit for bit
+    (conv_full, adjoint_apply, a short PG run) -- the reference recurses over any ndim
+    (convolution.hpp:55-74)."""
+    ref, orc = Oracle("ref"), Oracle("c")
+    g = np.random.Generator(np.random.PCG64(41))
+    for xs, hs in (((3, 4, 10, 12), (3, 1, 3, 5)), ((2, 3, 2, 8, 9), (1, 3, 3, 3, 5)),
+                   ((2, 3, 6, 7), (5, 3, 3, 3)), ((2, 2, 2, 2, 5, 6), (3, 1, 3, 1, 3, 3))):
+        x, h = g.uniform(0, 1, xs), g.uniform(-1, 1, hs)
+        y = ref.conv_full(x, h)
+        assert np.array_equal(orc.conv_full(x, h), y)
+        assert np.array_equal(orc.adjoint_apply(y, h, xs), ref.adjoint_apply(y, h, xs))
+        a = ref.deconv_pg(y, np.abs(h), xs, max_iters=5, tol_rel_objective=0.0, initial_step=1.0)
+        b = orc.deconv_pg(y, np.abs(h), xs, max_iters=5, tol_rel_objective=0.0, initial_step=1.0)
+        assert np.array_equal(a.estimate, b.estimate) and np.array_equal(a.objective_trace, b.objective_trace)
+
+
+def test_f32_restatement_tracks_the_reference(oracle_c, golden_solvers):
+    """oracle/pg_f32.py (deconv_pg in float32, the GPU tests' measure of what float32 can
+    resolve) follows the f64 reference on the golden random family to <= 2e-4, with the
+    same stop reasons, and reproduces the identity-kernel KATs exactly."""
+    from oracle.pg_f32 import deconv_pg_f32
+    d = golden_solvers
+    n = int(d["npg"])
+    for i in list(range(n - 5)) + [n - 5, n - 4, n - 3]:
+        cfg = d[f"pg_cfg{i}"]
+        xs = tuple(int(v) for v in d[f"pg_xs{i}"])
+        step = float(cfg[2]) if cfg[2] > 0 else oracle_c.estimate_step(d[f"pg_h{i}"], xs, 30)
+        x, tr, it, reason = deconv_pg_f32(d[f"pg_y{i}"], d[f"pg_h{i}"], xs, step, int(cfg[0]), float(cfg[1]))
+        assert reason == str(d[f"pg_stop{i}"]), i
+        assert _rel(x, d[f"pg_x{i}"]) <= 2e-4 or np.max(np.abs(x - d[f"pg_x{i}"])) <= 1e-6, i
