@@ -29,7 +29,19 @@ __global__ void __launch_bounds__(256, 2) k(const __grid_constant__ Taps taps, c
         const float4 v = *reinterpret_cast<const float4*>(rp + 4 * q);
         win[4 * q] = v.x; win[4 * q + 1] = v.y; win[4 * q + 2] = v.z; win[4 * q + 3] = v.w;
       }
-      if (MODE == 0) {
+      if (MODE == 2) {
+        // window-element-outer order: consecutive FFMAs share the window register (operand
+        // reuse cache), each accumulator still sums its taps in increasing kx order
+        const float* w = taps.t + ky * 34;
+#pragma unroll
+        for (int j = 0; j < 16 + KX - 1; ++j) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int kx = j - c;
+            if (kx >= 0 && kx < KX) acc[c] = fmaf(w[kx], win[j], acc[c]);
+          }
+        }
+      } else if (MODE == 0) {
         const float* w = taps.t + ky * 34;
 #pragma unroll
         for (int kx = 0; kx < KX; ++kx) {
@@ -74,6 +86,6 @@ template <int M> void run(const Taps& t, const float* in, float* out) {
 int main() {
   Taps t; for (int i = 0; i < KY * 34; ++i) t.t[i] = 0.001f * (i % 37);
   float *in, *out; cudaMalloc(&in, 4096*4); cudaMemset(in, 0, 4096*4); cudaMalloc(&out, 148*8*256*4);
-  run<0>(t, in, out); run<1>(t, in, out); run<0>(t, in, out); run<1>(t, in, out);
+  run<0>(t, in, out); run<1>(t, in, out); run<2>(t, in, out); run<0>(t, in, out); run<2>(t, in, out);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
