@@ -47,3 +47,18 @@ def rel_l2(a, b):
     den = np.linalg.norm(b.ravel())
     num = np.linalg.norm((a - b).ravel())
     return num / den if den > 0 else num
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With NDC_GUARD_BANDS=1 (guard-band mode, tests/test_gpu_guards.py) the whole run is a
+    memory check: any guard byte a device write changed in this process fails the session."""
+    if os.environ.get("NDC_GUARD_BANDS") != "1" or "paper_1711_11224_b200.ndconv" not in sys.modules:
+        return
+    from paper_1711_11224_b200 import ndconv
+    try:
+        bad = ndconv.guard_violations()
+    except Exception:  # library not loadable (CPU-only run)
+        return
+    print(f"\nguard bands: {bad} changed guard bytes in this session")
+    if bad:
+        session.exitstatus = 1
