@@ -119,8 +119,68 @@ __device__ __forceinline__ int stage_pos(int r, int q) { return r * kRX + 4 * (q
 
 // Epilogue value for `out` of quad q (4 columns) of one output row from the final
 // accumulators acc4 and the staged aux_in quad `in` (see EpiMode); reduction terms into
-// p0 / p1.  Columns past the valid extent are zero and excluded from the reductions.
+// p0 / p1.  Columns past the valid extent are zero and excluded from the reductions: the
+// reductions take the MASKED float32 values (a zero term leaves a sum or a max of
+// magnitudes unchanged), the max and the changed-count of the quad are formed in float32 /
+// int and folded into the float64 partials once -- same values bit for bit as per-element
+// float64 updates under `if (ok)`, without the selects on doubles those compile to.
 // MODE < 0: an intermediate tap chunk (the raw partial sum).
+template <int MODE>
+__device__ __forceinline__ float4 epilogue_res_lean(int cols_left, const float* acc4, const float* in, float sc,
+                                               float step, double& p0, double& p1) {
+  float res[4];
+  float qmax = 0.f;  // kEpiPG / kEpiKKT: max |min(x, g)| of the quad
+  int qcount = 0;    // kEpiPG: entries with trial != x
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const bool ok = c < cols_left;
+    const float acc_c = acc4[c];
+    float v = 0.f;
+    if (MODE < 0) {
+      v = acc_c;
+    } else if (MODE == kEpiStore) {
+      v = acc_c * sc;
+    } else if (MODE == kEpiResid) {
+      v = ok ? acc_c - in[c] : 0.f;
+      p0 += static_cast<double>(v) * static_cast<double>(v);
+    } else if (MODE == kEpiNorm) {
+      v = ok ? acc_c * sc : 0.f;
+      p0 += static_cast<double>(v) * static_cast<double>(v);
+    } else if (MODE == kEpiPG) {
+      // solvers.hpp:180-191: kkt = max|min(x,g)|, trial = max(x - step*g, 0), and the
+      // bitwise fixed-point test trial == x (g itself is the aux output).
+      const float gg = acc_c, xv = in[c];
+      float t = __fsub_rn(xv, __fmul_rn(gg, step));
+      t = t < 0.f ? 0.f : t;
+      v = t;
+      qmax = fmaxf(qmax, ok ? fabsf(fminf(xv, gg)) : 0.f);
+      qcount += (ok && t != xv) ? 1 : 0;
+    } else if (MODE == kEpiKKT) {
+      qmax = fmaxf(qmax, ok ? fabsf(fminf(in[c], acc_c)) : 0.f);
+    } else if (MODE == kEpiClamp) {
+      v = acc_c < 0.f ? 0.f : acc_c;
+    } else if (MODE == kEpiRLRatio) {
+      // tensor.hpp:112-116 guarded_div(y, A x) fused with the residual A x - y.
+      const float ax_v = acc_c * sc;
+      v = fabsf(ax_v) < 1e-12f ? 0.f : in[c] / ax_v;
+      const float d = ok ? ax_v - in[c] : 0.f;
+      p0 += static_cast<double>(d) * static_cast<double>(d);
+    } else if (MODE == kEpiRLUpdate) {
+      // solvers.hpp:290-291: x_next = x .* A^T(ratio); relative change terms.
+      const float xn = in[c] * acc_c;
+      v = xn;
+      const float xm = ok ? xn : 0.f, im = ok ? in[c] : 0.f;
+      const double d = static_cast<double>(xm) - static_cast<double>(im);
+      p0 += d * d;
+      p1 += static_cast<double>(im) * static_cast<double>(im);
+    }
+    res[c] = (ok || MODE < 0) ? v : 0.f;
+  }
+  if (MODE == kEpiPG || MODE == kEpiKKT) p0 = fmax(p0, static_cast<double>(qmax));
+  if (MODE == kEpiPG) p1 += static_cast<double>(qcount);
+  return make_float4(res[0], res[1], res[2], res[3]);
+}
+
 template <int MODE>
 __device__ __forceinline__ float4 epilogue_res(int cols_left, const float* acc4, const float* in, float sc,
                                                float step, double& p0, double& p1) {
@@ -187,15 +247,20 @@ __host__ __device__ constexpr bool mode_reads_aux() {
 
 // Warp-collective coalesced load of the strip's 32 rows x 16 columns into a staging
 // buffer (lanes 4r..4r+3 read row r: 8 whole 64-byte segments per instruction instead of
-// 32 half sectors); the epilogue then reads lane-per-row from shared memory.
-template <class RowOk, class RowOff>
-__device__ __forceinline__ void load_rows(float* wst, int lane, const float* src, RowOk row_ok, RowOff row_off) {
+// 32 half sectors); the epilogue then reads lane-per-row from shared memory.  `src0` points
+// at column 0 of the strip's first row, `rows` is how many of the 32 rows exist.  Row
+// r = 8k + (lane >> 2) of pass k: one running pointer (+ 8 rows per pass), and since
+// (r >> 1) & 3 does not depend on k, stage_pos(r, q) = stage_pos(lane >> 2, q) + 128 k.
+__device__ __forceinline__ void load_rows(float* wst, int lane, const float* src0, long long pitch, int rows) {
+  const int r0 = lane >> 2, q = lane & 3;
+  const float* p = src0 + static_cast<long long>(r0) * pitch + 4 * q;
+  float* w = wst + stage_pos(r0, q);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int r = 8 * k + (lane >> 2), q = lane & 3;
     float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row_ok(r)) x = *reinterpret_cast<const float4*>(src + row_off(r) + 4 * q);
-    *reinterpret_cast<float4*>(wst + stage_pos(r, q)) = x;
+    if (8 * k + r0 < rows) x = *reinterpret_cast<const float4*>(p);
+    *reinterpret_cast<float4*>(w + 8 * kRX * k) = x;
+    p += 8 * pitch;
   }
 }
 
@@ -203,14 +268,16 @@ __device__ __forceinline__ void load_rows(float* wst, int lane, const float* src
 // every store instruction covers 8 whole 64-byte row segments (lanes 4r..4r+3 -> row r),
 // so each 32-byte sector is written completely by one instruction.  (A lane-per-row
 // store writes half sectors, which the L2 fills from DRAM first: measured ~2x DRAM
-// traffic on small PSFs.)  row_ok(r) / row_off(r): validity and buffer offset of row r.
-template <class RowOk, class RowOff>
-__device__ __forceinline__ void store_rows(const float* wst, int lane, float* dst, RowOk row_ok, RowOff row_off) {
+// traffic on small PSFs.)  Arguments as for load_rows.
+__device__ __forceinline__ void store_rows(const float* wst, int lane, float* dst0, long long pitch, int rows) {
+  const int r0 = lane >> 2, q = lane & 3;
+  float* p = dst0 + static_cast<long long>(r0) * pitch + 4 * q;
+  const float* w = wst + stage_pos(r0, q);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int r = 8 * k + (lane >> 2), q = lane & 3;
-    const float4 x = *reinterpret_cast<const float4*>(wst + stage_pos(r, q));
-    if (row_ok(r)) *reinterpret_cast<float4*>(dst + row_off(r) + 4 * q) = x;
+    const float4 x = *reinterpret_cast<const float4*>(w + 8 * kRX * k);
+    if (8 * k + r0 < rows) *reinterpret_cast<float4*>(p) = x;
+    p += 8 * pitch;
   }
 }
 
@@ -239,8 +306,9 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
   for (int j = 0; j < RY; ++j) {
     const int row0 = wrow0 + 32 * j;  // the warp's first row of block j
     const bool mine = row0 + lane < g.out_ey && strip_ok;
-    auto row_ok = [&](int r) { return strip_ok && row0 + r < g.out_ey; };
-    auto row_off = [&](int r) { return obase + static_cast<long long>(row0 + r) * g.out_pitch; };
+    // staged loads / stores: offset of the block's first row, and how many of its rows exist
+    const long long blk = obase + static_cast<long long>(row0) * g.out_pitch;
+    const int rows = strip_ok ? g.out_ey - row0 : 0;
     float* acc_j = acc[j];
     if (!STAGED) {
       const long long o = obase + static_cast<long long>(row0 + lane) * g.out_pitch;
@@ -280,7 +348,7 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
       continue;
     }
     if (g.accum) {  // partial sums of the earlier tap chunks
-      load_rows(wst, lane, a.accum_in, row_ok, row_off);
+      load_rows(wst, lane, a.accum_in + blk, g.out_pitch, rows);
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < kRX / 4; ++q) {
@@ -298,7 +366,7 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
       if (wpre != nullptr) {
         if (j == 0) cp_async_wait_all();
       } else {
-        load_rows(wst, lane, a.aux_in, row_ok, row_off);
+        load_rows(wst, lane, a.aux_in + blk, g.out_pitch, rows);
       }
       __syncwarp();
     }
@@ -314,12 +382,12 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
         in[4 * q + 3] = v.w;
       }
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (mine) r = epilogue_res<MODE>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
+      if (mine) r = epilogue_res_lean<MODE>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
       if (kStoreOut) *reinterpret_cast<float4*>(wst + sp) = r;  // same lane, same slot
     }
     if (kStoreOut) {
       __syncwarp();
-      store_rows(wst, lane, a.out, row_ok, row_off);
+      store_rows(wst, lane, a.out + blk, g.out_pitch, rows);
       __syncwarp();
     }
     if (kStoreAux) {  // kEpiPG: g = acc; kEpiRLRatio: A x - Y
@@ -334,7 +402,7 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
         *reinterpret_cast<float4*>(wst + stage_pos(lane, q)) = make_float4(r[0], r[1], r[2], r[3]);
       }
       __syncwarp();
-      store_rows(wst, lane, a.aux_out, row_ok, row_off);
+      store_rows(wst, lane, a.aux_out + blk, g.out_pitch, rows);
       __syncwarp();
     }
   }
@@ -521,6 +589,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
                      const __grid_constant__ TapBlock taps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int TY = 64 * RY;
+  constexpr bool kStagedEpi = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX;
 
   const int b = blockIdx.z;
   if (a.active != nullptr && a.active[b] == 0) return;
@@ -636,16 +705,16 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     const long long obase = static_cast<long long>(b) * g.out_image +
                             static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
     if (ox0 < g.out_ex) {
+      // row 8k + (lane >> 2) of block j: one running pointer, stage_pos(r, q) = stage_pos(r0, q) + 128 k
+      const int r0 = lane >> 2, q = lane & 3;
+      const int row_first = ty0 + wy * (32 * RY) + r0;
+      const float* src = a.aux_in + obase + static_cast<long long>(row_first) * g.out_pitch + 4 * q;
+      float* dst = pre + stage_pos(r0, q);
 #pragma unroll
-      for (int j = 0; j < RY; ++j)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = 8 * k + (lane >> 2), q = lane & 3;
-          const int row = ty0 + wy * (32 * RY) + 32 * j + r;
-          if (row < g.out_ey)
-            cp_async16(pre + j * (32 * kRX) + stage_pos(r, q),
-                       a.aux_in + obase + static_cast<long long>(row) * g.out_pitch + 4 * q);
-        }
+      for (int k = 0; k < 4 * RY; ++k) {
+        if (row_first + 8 * k < g.out_ey) cp_async16(dst + 8 * kRX * k, src);
+        src += 8 * g.out_pitch;
+      }
     }
     cp_async_commit();
     wpre = pre;
@@ -664,8 +733,21 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
   if (EDGE && compact) nrun = 1;  // rows 0..15 of block 0 only; inactive lanes are masked at the end
   for (int i = 0; i < n; ++i) {
-    const int s = i % g.stages;
-    mbar_wait(&bars[s], static_cast<uint32_t>((i / g.stages) & 1));
+    // ring slot and mbarrier parity of staged plane i (a runtime i % stages and i / stages
+    // cost ~40 instructions per plane; plans use one or two stages)
+    int s;
+    uint32_t parity;
+    if (g.stages == 2) {
+      s = i & 1;
+      parity = static_cast<uint32_t>(i >> 1) & 1u;
+    } else if (g.stages == 1) {
+      s = 0;
+      parity = static_cast<uint32_t>(i) & 1u;
+    } else {
+      s = i % g.stages;
+      parity = static_cast<uint32_t>(i / g.stages) & 1u;
+    }
+    mbar_wait(&bars[s], parity);
     const float* base =
         EDGE ? reinterpret_cast<const float*>(smem_raw + s * sbytes) + lane_row * g.pitch_s + lane_col
              : reinterpret_cast<const float*>(smem_raw + s * sbytes) + (wy * (32 * RY) + lane) * g.pitch_s + wx * kRX;
@@ -752,7 +834,8 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     // fixed order, so the result stays deterministic)
     const bool pmax = p0_is_max(g.mode);
     p0 = pmax ? warp_max(p0) : warp_sum(p0);
-    p1 = warp_sum(p1);
+    // (staged kernels: only the modes that produce p1 reduce it; the others leave it 0)
+    if (!kStagedEpi || g.mode == kEpiPG || g.mode == kEpiRLUpdate) p1 = warp_sum(p1);
     if (lane == 0) {
       const long long idx =
           ((static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile) *
