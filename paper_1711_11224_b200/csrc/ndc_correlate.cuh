@@ -291,8 +291,8 @@ __device__ __forceinline__ void store_rows(const float* wst, int lane, float* ds
 // config 2, the direct form ~30 % slower on 3x3 / 5x5 PSFs).
 template <int MODE, int RY, bool STAGED>
 __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs& a, int b, int oz, int ox0,
-                                              int wrow0, int lane, float (&acc)[RY][kRX], float* wst,
-                                              const float* wpre, double& p0, double& p1) {
+                                              int wrow0, int lane, float (&acc)[RY][kRX], float* wst0,
+                                              int wst_stride, const float* wpre, double& p0, double& p1) {
   constexpr bool kReadsAux = mode_reads_aux<MODE>();
   constexpr bool kStoreOut = MODE != kEpiKKT;
   constexpr bool kStoreAux = MODE == kEpiPG || MODE == kEpiRLRatio;
@@ -310,6 +310,9 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
     const long long blk = obase + static_cast<long long>(row0) * g.out_pitch;
     const int rows = strip_ok ? g.out_ey - row0 : 0;
     float* acc_j = acc[j];
+    // staging buffer of block j: the warp's 2 KB buffer, or (wst_stride != 0) the block's own
+    // operand-prefetch buffer, which each lane has read its slot of before it overwrites it
+    float* wst = wst0 + j * wst_stride;
     if (!STAGED) {
       const long long o = obase + static_cast<long long>(row0 + lane) * g.out_pitch;
       if (!mine) continue;
@@ -542,7 +545,7 @@ __device__ __forceinline__ void accumulate_rows(RowAcc<PK> (&acc)[RY], const flo
 #define NDC_MIN_BLOCKS 2
 #endif
 #ifndef NDC_SMALL_MIN_BLOCKS
-#define NDC_SMALL_MIN_BLOCKS 4
+#define NDC_SMALL_MIN_BLOCKS 5
 #endif
 #ifndef NDC_STAGED_KX
 #define NDC_STAGED_KX kStagedMaxKX  // staged (coalesced) epilogue up to this kernel x-extent
@@ -675,7 +678,13 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
 
   const int sbytes = stage_bytes_aligned(g.rows, g.pitch_s);
   constexpr bool kStaging = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX || !NDC_NOSTAGING_DIRECT;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + barrier_offset(g.stages, sbytes, kStaging));
+  // Launches that prefetch the epilogue operand (single-plane small PSFs) carry per-warp
+  // prefetch buffers after the barriers; those double as the staging buffers, so such a
+  // launch has no separate staging area (16 KB less per CTA).
+  const bool prebuf = KX <= NDC_PREFETCH_KX && g.aux_prefetch;
+  const int bar_off = barrier_offset(g.stages, sbytes, kStaging && !prebuf);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + bar_off);
+  float* const wbuf = reinterpret_cast<float*>(smem_raw + bar_off + 128) + warp * (RY * 32 * kRX);
   const uint32_t tx_bytes = static_cast<uint32_t>(g.rows * g.pitch_s * 4);
 
   if (tid == 0) {
@@ -697,10 +706,9 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
   // Small PSFs: prefetch the epilogue's aux_in strip (Y or x) into shared memory now,
   // so it arrives during the FFMA loop instead of stalling the epilogue.
   const float* wpre = nullptr;
-  if (KX <= NDC_PREFETCH_KX && g.aux_prefetch && g.final_chunk && mode_reads_aux_rt(g.mode) && phase == 0 &&
-      !(EDGE && compact)) {
-    float* pre = reinterpret_cast<float*>(smem_raw + barrier_offset(g.stages, sbytes, kStaging) + 128) +
-                 warp * (RY * 32 * kRX);
+  // (not with earlier tap chunks to add: their partial sums are staged through the same buffer)
+  if (prebuf && g.final_chunk && !g.accum && mode_reads_aux_rt(g.mode) && phase == 0 && !(EDGE && compact)) {
+    float* pre = wbuf;
     const int ox0 = tx0 + wx * kRX;
     const long long obase = static_cast<long long>(b) * g.out_image +
                             static_cast<long long>(g.out_z0 + oz) * g.out_plane + ox0;
@@ -804,17 +812,18 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
   }
 
   // ---- epilogue (one instantiation per mode: the dispatch happens once per tile) --------
-  float* wst = reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
+  float* wst = prebuf ? wbuf : reinterpret_cast<float*>(smem_raw + g.stages * sbytes) + warp * (32 * kRX);
+  const int wst_stride = prebuf ? 32 * kRX : 0;
   double p0 = 0.0, p1 = 0.0;
   // (compact edge tiles: per-lane row / strip, so the lane-per-row direct epilogue; its
   // row is wrow0 + lane, hence the per-lane wrow0)
 #define NDC_EPI(M)                                                                                      \
   if (EDGE && compact)                                                                                \
-    epilogue_tile<M, RY, false>(g, a, b, oz, tx0 + lane_col, ty0 + lane_row - lane, lane, acc, wst, nullptr, \
+    epilogue_tile<M, RY, false>(g, a, b, oz, tx0 + lane_col, ty0 + lane_row - lane, lane, acc, wst, 0, nullptr, \
                                 p0, p1);                                                                \
   else                                                                                                \
     epilogue_tile<M, RY, (KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX)>(g, a, b, oz, tx0 + wx * kRX, ty0 + wy * (32 * RY), lane, acc, \
-                                               wst, wpre, p0, p1)
+                                               wst, wst_stride, wpre, p0, p1)
   switch (phase != 0 ? -2 : g.final_chunk ? g.mode : -1) {  // -2: folded into a phase-0 warp
     case kEpiStore: NDC_EPI(kEpiStore); break;
     case kEpiResid: NDC_EPI(kEpiResid); break;
@@ -850,8 +859,10 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
                       const TapBlock& taps, int batch, int nz_out, cudaStream_t s, cudaStream_t s_edge) {
   // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
   constexpr bool kStaging = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX || !NDC_NOSTAGING_DIRECT;
-  const size_t smem = correlate_smem_bytes(g, kStaging) +
-                      ((KX <= NDC_PREFETCH_KX && g.aux_prefetch) ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
+  // (launches with the per-warp operand-prefetch buffers stage their stores through them)
+  const bool prebuf = KX <= NDC_PREFETCH_KX && g.aux_prefetch;
+  const size_t smem = correlate_smem_bytes(g, kStaging && !prebuf) +
+                      (prebuf ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
   // packed FFMA2 tap loop (see pack_mode): edge tiles only where it is always on
   constexpr int kPM = pack_mode<KX>();
   constexpr bool kPkFull = kPM != kPackNever, kPkEdge = kPM == kPackAlways;

@@ -25,7 +25,10 @@ for name in a.configs:
     B, xs = SHAPES[name] if name in SHAPES else (16, (2048, 2048))  # c2k<N>: N x N Gaussian
     if name.startswith("c2b"):  # c2b<N>: config 2 with a batch of N images (wave-tail sizing)
         B, name = int(name[3:]), "c2"
-    if name == "c2k1":
+    if name.startswith("c3k"):  # c3k<N>: N x N x N Gaussian on a 256 x 512 x 512 volume
+        B, xs = 1, (256, 512, 512)
+        h = synth.gaussian_psf((int(name[3:]),) * 3, 1.0)
+    elif name == "c2k1":
         h = np.ones((1, 1))
     elif name.startswith("c2k"):
         h = synth.gaussian_psf((int(name[3:]),) * 2, 1.0)
