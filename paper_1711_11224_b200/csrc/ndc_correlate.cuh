@@ -51,6 +51,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// Named CTA barrier `id`, split into its two halves: the warps that only signal (arrive,
+// non-blocking) and the warp that waits for all `count` threads (sync).
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("barrier.cta.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2) {
   asm volatile(
@@ -765,7 +774,20 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     else if (RY > 1 && nrun == 1)
       accumulate_rows<KX, SH, RY, 1, EDGE, PK>(acc2, base, trow, g.KY, phase, nph, g.pitch_s);
     if (i + g.stages < n) {
-      __syncthreads();  // every warp is done with stage s before it is refilled
+      // Every warp is done with stage s before it is refilled.  Edge tiles: their warps split
+      // the tap rows unevenly (15 rows over 4 phases: 4 / 4 / 4 / 3), so only warp 0, which
+      // issues the refill, waits (named barrier 1 + s); the others signal and go on to the
+      // next stage (ncu, config 3 edge launch: barrier stalls 1.2 per issued instruction).
+      // The full-tile kernels keep the plain barrier: with any split form ptxas moves
+      // config 4's tap loads off the uniform datapath (profiles/r02e_tap_loop_probes.md).
+      if constexpr (EDGE) {
+        if (warp != 0)
+          bar_arrive(1 + s, kThreads);
+        else
+          bar_sync(1 + s, kThreads);
+      } else {
+        __syncthreads();
+      }
       if (tid == 0) {
         const int iz = oz + kzA + i + g.stages + g.off_z;
         mbar_expect_tx(&bars[s], tx_bytes);
