@@ -134,7 +134,8 @@ __device__ __forceinline__ int stage_pos(int r, int q) { return r * kRX + 4 * (q
 // int and folded into the float64 partials once -- same values bit for bit as per-element
 // float64 updates under `if (ok)`, without the selects on doubles those compile to.
 // MODE < 0: an intermediate tap chunk (the raw partial sum).
-template <int MODE>
+// FULL: all four columns are inside the output (no column masks at all).
+template <int MODE, bool FULL = false>
 __device__ __forceinline__ float4 epilogue_res_lean(int cols_left, const float* acc4, const float* in, float sc,
                                                float step, double& p0, double& p1) {
   float res[4];
@@ -142,7 +143,7 @@ __device__ __forceinline__ float4 epilogue_res_lean(int cols_left, const float* 
   int qcount = 0;    // kEpiPG: entries with trial != x
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const bool ok = c < cols_left;
+    const bool ok = FULL || c < cols_left;
     const float acc_c = acc4[c];
     float v = 0.f;
     if (MODE < 0) {
@@ -383,20 +384,30 @@ __device__ __forceinline__ void epilogue_tile(const CorrGeom& g, const CorrArgs&
       __syncwarp();
     }
     float in[kRX];
+    // (strips wholly inside the output -- all but the last tile column -- take the
+    // instantiation without column masks)
+    auto block_math = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
 #pragma unroll
-    for (int q = 0; q < kRX / 4; ++q) {
-      const int sp = stage_pos(lane, q);
-      if (kReadsAux) {
-        const float4 v = *reinterpret_cast<const float4*>(src_in + sp);
-        in[4 * q] = v.x;
-        in[4 * q + 1] = v.y;
-        in[4 * q + 2] = v.z;
-        in[4 * q + 3] = v.w;
+      for (int q = 0; q < kRX / 4; ++q) {
+        const int sp = stage_pos(lane, q);
+        if (kReadsAux) {
+          const float4 v = *reinterpret_cast<const float4*>(src_in + sp);
+          in[4 * q] = v.x;
+          in[4 * q + 1] = v.y;
+          in[4 * q + 2] = v.z;
+          in[4 * q + 3] = v.w;
+        }
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (mine)
+          r = epilogue_res_lean<MODE, kFull>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
+        if (kStoreOut) *reinterpret_cast<float4*>(wst + sp) = r;  // same lane, same slot
       }
-      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (mine) r = epilogue_res_lean<MODE>(cols_left - 4 * q, &acc_j[4 * q], &in[4 * q], sc, step, p0, p1);
-      if (kStoreOut) *reinterpret_cast<float4*>(wst + sp) = r;  // same lane, same slot
-    }
+    };
+    if (RY == 1 && cols_left >= kRX)  // (the 128-row kernels measured 0.5 % slower with both copies)
+      block_math(std::true_type{});
+    else
+      block_math(std::false_type{});
     if (kStoreOut) {
       __syncwarp();
       store_rows(wst, lane, a.out + blk, g.out_pitch, rows);
@@ -602,12 +613,20 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int TY = 64 * RY;
   constexpr bool kStagedEpi = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX;
+  // 64-row staged kernels (the HBM-bound small PSFs): single-plane launches come as a 2-D
+  // grid of tiles (bit 1 of g.aux_prefetch; no tile-index division) and skip the plane ring
+  constexpr bool kLean2D = kStagedEpi && RY == 1 && !EDGE;
+  const bool grid2d = kLean2D && (g.aux_prefetch & 2) != 0;
 
   const int b = blockIdx.z;
   if (a.active != nullptr && a.active[b] == 0) return;
   int oz = blockIdx.y;
   int txi, tyi;
-  if (!EDGE) {
+  if (!EDGE && grid2d) {
+    oz = 0;
+    txi = blockIdx.x;
+    tyi = blockIdx.y;
+  } else if (!EDGE) {
     int t = blockIdx.x;
     if (NDC_Z_FAST && gridDim.y > 1) {
       // 3-D: consecutive CTAs take consecutive output planes of one tile position, so the
@@ -690,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
   // Launches that prefetch the epilogue operand (single-plane small PSFs) carry per-warp
   // prefetch buffers after the barriers; those double as the staging buffers, so such a
   // launch has no separate staging area (16 KB less per CTA).
-  const bool prebuf = KX <= NDC_PREFETCH_KX && g.aux_prefetch;
+  const bool prebuf = KX <= NDC_PREFETCH_KX && (g.aux_prefetch & 1) != 0;
   const int bar_off = barrier_offset(g.stages, sbytes, kStaging && !prebuf);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + bar_off);
   float* const wbuf = reinterpret_cast<float*>(smem_raw + bar_off + 128) + warp * (RY * 32 * kRX);
@@ -749,6 +768,13 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     if (ty0 + wy * (32 * RY) + 32 * j < g.out_ey) nrun = j + 1;
   if (tx0 + wx * kRX >= g.out_ex) nrun = 0;
   if (EDGE && compact) nrun = 1;  // rows 0..15 of block 0 only; inactive lanes are masked at the end
+  if (grid2d) {  // one plane, one stage
+    mbar_wait(&bars[0], 0u);
+    if (nrun != 0) {
+      const float* base = reinterpret_cast<const float*>(smem_raw) + (wy * (32 * RY) + lane) * g.pitch_s + wx * kRX;
+      accumulate_rows<KX, SH, RY, RY, EDGE, PK>(acc2, base, taps.t, g.KY, phase, nph, g.pitch_s);
+    }
+  } else
   for (int i = 0; i < n; ++i) {
     // ring slot and mbarrier parity of staged plane i (a runtime i % stages and i / stages
     // cost ~40 instructions per plane; plans use one or two stages)
@@ -869,7 +895,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
     if (!kStagedEpi || g.mode == kEpiPG || g.mode == kEpiRLUpdate) p1 = warp_sum(p1);
     if (lane == 0) {
       const long long idx =
-          ((static_cast<long long>(b) * gridDim.y + oz) * (g.tiles_x * g.tiles_y) + tile) *
+          ((static_cast<long long>(b) * (grid2d ? 1 : gridDim.y) + oz) * (g.tiles_x * g.tiles_y) + tile) *
               (kThreads / 32) + warp;
       a.partials[idx] = make_double2(p0, p1);
     }
@@ -882,7 +908,7 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
   // staged (small-PSF) kernels add the per-warp aux_in prefetch buffers
   constexpr bool kStaging = KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX || !NDC_NOSTAGING_DIRECT;
   // (launches with the per-warp operand-prefetch buffers stage their stores through them)
-  const bool prebuf = KX <= NDC_PREFETCH_KX && g.aux_prefetch;
+  const bool prebuf = KX <= NDC_PREFETCH_KX && (g.aux_prefetch & 1) != 0;
   const size_t smem = correlate_smem_bytes(g, kStaging && !prebuf) +
                       (prebuf ? 128 + (kThreads / 32) * RY * 32 * kRX * 4 : 0);
   // packed FFMA2 tap loop (see pack_mode): edge tiles only where it is always on
@@ -911,11 +937,20 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
   const int n_full = g.full_tx * g.full_ty;
   const int n_edge = g.tiles_x * g.tiles_y - n_full;
   if (n_full > 0) {
-    const dim3 grid(n_full, nz_out, batch);
+    dim3 grid(n_full, nz_out, batch);
+    // 64-row staged kernels, single-plane launch: a 2-D grid of tiles (see kLean2D)
+    constexpr bool kLean2D = (KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX) && RY == 1;
+    CorrGeom g2 = g;
+    // (exactly one staged plane per tile: kzA = 0, n = 1 in the kernel)
+    if (kLean2D && nz_out == 1 && g.in_ez == 1 && g.kz0 == 0 && g.kz1 == 1 && g.stages == 1 && g.off_z == 0 &&
+        g.full_ty <= 65535) {
+      g2.aux_prefetch |= 2;
+      grid = dim3(g.full_tx, g.full_ty, batch);
+    }
     if (pk)
-      correlate_kernel<KX, SH, RY, false, kPkFull><<<grid, kThreads, smem, s>>>(map, g, a, taps);
+      correlate_kernel<KX, SH, RY, false, kPkFull><<<grid, kThreads, smem, s>>>(map, g2, a, taps);
     else
-      correlate_kernel<KX, SH, RY, false, false><<<grid, kThreads, smem, s>>>(map, g, a, taps);
+      correlate_kernel<KX, SH, RY, false, false><<<grid, kThreads, smem, s>>>(map, g2, a, taps);
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
   }
   if (n_edge > 0)

@@ -76,7 +76,8 @@ struct CorrGeom {
   int full_tx, full_ty;  // tile columns / rows wholly inside the output
   int rows, pitch_s;   // shared tile: rows x pitch_s floats per stage
   int stages;
-  int aux_prefetch;    // cp.async the epilogue's aux_in strip at kernel start (small PSFs)
+  int aux_prefetch;    // bit 0: cp.async the epilogue's aux_in strip at kernel start (small PSFs);
+                       // bit 1 (set by the launcher): single-plane launch as a 2-D grid of tiles
   int accum;           // add the partial sum held in `accum_in`
   int mode;            // EpiMode (ignored unless final)
   int final_chunk;     // last tap chunk: apply the epilogue
