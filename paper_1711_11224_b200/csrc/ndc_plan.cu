@@ -183,11 +183,8 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
   kcx_ = KX_ <= kMaxKX ? KX_ : kMaxKX;
   // Two output rows per thread (tile height 128) halves the per-row tap loads and loop
   // overhead; used for single-plane (2-D / batched) problems whose 128+KY-1 staged rows
-  // fit one TMA box.  3-D volumes keep 64-row tiles so two plane stages fit beside a
-  // second CTA per SM.
-  // For 3-D volumes two plane stages must also leave room for two CTAs per SM
-  // (measured: RY=2 wins on config 4's 21x9x9 PSF, loses on configs 3 and 5 whose
-  // 128-row stages would drop residency to one CTA).
+  // fit one TMA box.  For 3-D volumes two 128-row plane stages must also leave room for two
+  // CTAs per SM (configs 3 and 4); otherwise see the one-stage rule below (config 5).
   stages_ = (KZ_ > 1) ? 2 : 1;
   {
     const long long pitch2 = std::max(shared_pitch_for(kcx_, 0), shared_pitch_for(kcx_, 2));
@@ -198,8 +195,17 @@ Plan::Plan(int device, size_t batch, int ndim, const size_t* x_ext, const size_t
     // adjoint +2 %, forward unchanged)
     const long long budget = (kcx_ <= kStagedMaxKX ? 90 : 110) * 1024LL;
     ry_ = (fits && (KZ_ == 1 || stages_ * stage2 <= budget)) ? 2 : 1;
-    // small PSFs are HBM-bound: 64-row tiles at 4 CTAs / SM keep more loads in flight
+    // small PSFs are HBM-bound: 64-row tiles at 5 CTAs / SM keep more loads in flight
     if (KX_ <= kSmallMaxKX) ry_ = 1;
+    // Wide 3-D PSFs whose two 128-row stages do not fit: ONE 128-row stage per CTA and three
+    // CTAs / SM (the scalar direct-epilogue kernels of KX >= 23 run at 80 registers) beat
+    // 64-row tiles on a two-stage ring at two CTAs / SM -- two rows per lane share every tap
+    // load, and a CTA's wait for its next plane hides behind the other two.  Config 5
+    // (65 x 33 x 33): forward +3.0 %, adjoint +1.4 % (profiles/r02i_c5_tiles.txt).
+    if (KZ_ > 1 && ry_ == 1 && fits && kcx_ >= 23 && 3 * (stage2 + 1024) <= 225 * 1024LL) {
+      ry_ = 2;
+      stages_ = 1;
+    }
   }
   kcy_ = std::min(KY_, kMaxRows - kTileY * ry_ + 1);  // staged rows 64*ry + kcy - 1 <= TMA box limit
 
