@@ -111,9 +111,11 @@ __host__ __device__ constexpr int stage_bytes_aligned(int rows, int pitch_s) {
 // stages, so no warp ever waits for another around the epilogue.
 constexpr int kStagingBytes = (kThreads / 32) * 32 * kRX * 4;
 
-// Dynamic shared memory: stages, staging (staged-epilogue kernels only), then the stage
-// mbarriers.  The direct-epilogue (large-PSF) kernels carry no staging buffer: 16 KB less
-// per CTA lets a third CTA share the SM when registers allow (config 2: 3 x 63 KB).
+// Dynamic shared memory: stages, staging (staged-epilogue kernels without operand-prefetch
+// buffers only), the stage mbarriers, then -- single-plane small PSFs -- the per-warp
+// operand-prefetch buffers, which double as the staging buffers.  The direct-epilogue
+// (large-PSF) kernels carry no staging buffer: 16 KB less per CTA lets a third CTA share
+// the SM when registers allow (configs 2 and 5: 3 x 63-64 KB).
 __host__ __device__ constexpr int barrier_offset(int stages, int sbytes, bool staging) {
   return stages * sbytes + (staging ? kStagingBytes : 0);
 }

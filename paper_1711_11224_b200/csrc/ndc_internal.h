@@ -34,7 +34,7 @@ constexpr int kMaxStages = 3;
 constexpr int kMaxDims = 8;  // tensor dimensions accepted (4+ merge into the plane axis)
 // HBM-bound small PSFs (ndc_correlate.cuh): kernel x-extents up to kStagedMaxKX use the
 // staged, sector-complete epilogue (and, for single-plane problems, a cp.async prefetch
-// of the epilogue's aux_in strip); up to kSmallMaxKX also 64-row tiles at 4 CTAs / SM.
+// of the epilogue's aux_in strip); up to kSmallMaxKX also 64-row tiles at 5 CTAs / SM.
 constexpr int kStagedMaxKX = 9;
 constexpr int kSmallMaxKX = 5;
 // Single-plane PSFs up to kPrefetchMaxKX prefetch the epilogue's aux_in strip with

@@ -1,5 +1,6 @@
 """Instructions executed per source line and warp from an `ncu --set full --import-source on`
-report: python tools/ncu_lines.py report.ncu-rep [block] [warps]  (block: 1-based function index)."""
+report: python tools/ncu_lines.py report.ncu-rep [block] [warps]  (block: 1-based function index;
+warps: divide by the launch's warp count for per-warp figures).  Captures: tools/ncu_run_cfg.py."""
 import collections
 import csv
 import io

@@ -1,3 +1,6 @@
+"""Two forward + adjoint passes of a BASELINE-shaped plan on zero inputs, for ncu captures of a
+single launch (`ncu --set full --import-source on -k regex:correlate -s N -c 1 python
+tools/ncu_run_cfg.py c4s`, then tools/ncu_lines.py on the report)."""
 import sys, numpy as np
 sys.path.insert(0, ".")
 from paper_1711_11224_b200 import ndconv as nd, synth
