@@ -20,10 +20,10 @@ LIB = os.path.join(PKG, "libndconv_b200.so")
 CLI = os.path.join(PKG, "ndconv")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
-SOURCES = ["ndc_corr_sh0_ry1.cu", "ndc_corr_sh0_ry2.cu", "ndc_corr_sh2_ry1.cu", "ndc_corr_sh2_ry2.cu",
+SOURCES = ["ndc_corr_sh0_ry1.cu", "ndc_corr_sh0_ry2.cu", "ndc_corr_sh2_ry1.cu", "ndc_corr_sh2_ry2.cu", "ndc_corr_pair.cu",
            "ndc_kernels.cu", "ndc_plan.cu", "ndc_capi.cu", "ndc_comm.cu", "ndc_io.cu", "ndc_sim.cu",
            "ndc_probe.cu"]
-HEADERS = ["ndc_internal.h", "ndc_plan.h", "ndc_correlate.cuh", "ndc_io.h", "ndc_sim.h", os.path.join("..", "..", "include", "ndconv_b200.h")]
+HEADERS = ["ndc_internal.h", "ndc_plan.h", "ndc_correlate.cuh", "ndc_correlate_pair.cuh", "ndc_io.h", "ndc_sim.h", os.path.join("..", "..", "include", "ndconv_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                 "-Xptxas", "-v", "-I", os.path.join(PKG, "..", "include")]

@@ -938,7 +938,11 @@ cudaError_t launch_kx(const CUtensorMap& map, const CorrGeom& g, const CorrArgs&
   // full tiles, then the partial last tile column / row
   const int n_full = g.full_tx * g.full_ty;
   const int n_edge = g.tiles_x * g.tiles_y - n_full;
-  if (n_full > 0) {
+  // narrow 3-D PSFs: two output planes per CTA (ndc_correlate_pair.cuh)
+  constexpr bool kPairKernel = RY == 2 && (KX == 7 || KX == 9);
+  if (kPairKernel && n_full > 0 && nz_out >= 2 && g.kz1 - g.kz0 >= 2 && !pk) {
+    if (cudaError_t e = launch_correlate_pair(KX, SH, map, g, a, taps, batch, nz_out, s); e != cudaSuccess) return e;
+  } else if (n_full > 0) {
     dim3 grid(n_full, nz_out, batch);
     // 64-row staged kernels, single-plane launch: a 2-D grid of tiles (see kLean2D)
     constexpr bool kLean2D = (KX <= NDC_STAGED_KX || KX <= NDC_PREFETCH_KX) && RY == 1;

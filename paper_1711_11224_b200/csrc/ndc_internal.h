@@ -123,6 +123,10 @@ NDC_DECL_CORR(0, 2)
 NDC_DECL_CORR(2, 1)
 NDC_DECL_CORR(2, 2)
 #undef NDC_DECL_CORR
+// Full tiles of a 3-D launch with two output planes per CTA (ndc_correlate_pair.cuh):
+// narrow PSFs (kx = 7, 9) on 128-row tiles.
+cudaError_t launch_correlate_pair(int kx, int sh, const CUtensorMap& map, const CorrGeom& g, const CorrArgs& a,
+                                  const TapBlock& taps, int batch, int nz_out, cudaStream_t s);
 size_t correlate_smem_bytes(const CorrGeom& g, bool staging);
 int shared_pitch_for(int kx, int sh);
 

@@ -220,6 +220,34 @@ def test_edge_tiles_few_rows(nd, oracle_c, xs, hs):
     np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
 
 
+@pytest.mark.parametrize("xs,hs", [((13, 140, 70), (5, 9, 9)), ((6, 130, 130), (3, 7, 7)), ((7, 260, 70), (4 * 2 + 1, 9, 7)),
+                                   ((13, 140, 70), (31, 31, 9)), ((1, 130, 70), (3, 9, 9)), ((2, 130, 70), (21, 9, 9))])
+def test_two_planes_per_cta(nd, oracle_c, xs, hs):
+    """Narrow 3-D PSFs (x-extent 7 or 9) on 128-row tiles run their full tiles two output planes
+    per CTA (ndc_correlate_pair.cuh): odd and even plane counts, PSFs deeper than the volume
+    (most staged planes meet only one of the two planes), a PSF of two tap chunks (31 x 31 x 9:
+    24 + 7 slices accumulated through the scratch volume), and a single-plane volume whose
+    adjoint falls back to the general kernel; every element of forward and adjoint and a short
+    PG run against the oracle."""
+    rng = np.random.default_rng(sum(xs) + 7 * sum(hs))
+    x = rng.uniform(0, 1, xs)
+    h = rng.uniform(0, 1, hs)
+    h /= h.sum()
+    y_ref = oracle_c.conv_full(x, h)
+    y = nd.conv_full(x, h)
+    assert np.max(np.abs(y - y_ref)) <= 1e-5 * np.max(np.abs(y_ref))
+    r = rng.uniform(-1, 1, y_ref.shape)
+    a_ref = oracle_c.adjoint_apply(r, h, xs)
+    assert np.max(np.abs(nd.adjoint_apply(r, h, xs) - a_ref)) <= 1e-5 * np.max(np.abs(a_ref))
+    yo = y_ref + rng.uniform(0, 1e-3, y_ref.shape)
+    cfg = nd.DeconvConfig(max_iters=3, tol_rel_objective=0.0, initial_step=1.0)
+    got = nd.deconv_pg(yo, h, xs, cfg)
+    want = oracle_c.deconv_pg(yo, h, xs, max_iters=3, tol_rel_objective=0.0, initial_step=1.0)
+    assert got.iterations_run == want.iterations_run
+    assert rel_l2(got.estimate, want.estimate) <= 1e-4
+    np.testing.assert_allclose(got.objective_trace, want.objective_trace, rtol=1e-4)
+
+
 @pytest.mark.parametrize("xs,hs", [((130, 150), (7, 7)), ((150, 130), (9, 9)), ((140, 140), (11, 11)),
                                    ((129, 200), (13, 13)), ((200, 129), (17, 17)), ((150, 160), (21, 21)),
                                    ((5, 70, 90), (3, 9, 9)), ((5, 70, 90), (3, 11, 19)), ((4, 64, 64), (3, 7, 7))])
