@@ -52,7 +52,7 @@ def parse(cfg, csv_path, counts_path):
     ki, ni, vi, idi = head.index("Kernel Name"), head.index("Metric Name"), head.index("Metric Value"), head.index("ID")
     per = {}
     for r in rows[1:]:
-        if len(r) <= max(ki, ni, vi) or "correlate_kernel" not in r[ki]:
+        if len(r) <= max(ki, ni, vi) or "correlate" not in r[ki]:  # correlate_kernel, correlate_pair_kernel
             continue
         d = per.setdefault(int(r[idi]), {})
         d[r[ni]] = float(r[vi].replace(",", ""))
