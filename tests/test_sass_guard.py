@@ -26,7 +26,8 @@ EXPECT = {
     (31, 2, 0): 1.0,   # c2 (31x31)
     (15, 2, 1): 1.0,   # c3 (15x15 in-plane, packed FFMA2)
     (9, 2, 0): 1.0,    # c4 (9x9 in-plane)
-    (33, 1, 0): 0.80,  # c5 (33x33 in-plane, 64-row tiles)
+    (33, 2, 0): 1.0,   # c5 (33x33 in-plane, 128-row tiles on one stage)
+    (33, 1, 0): 0.80,  # 33-wide PSFs too tall for a 128-row TMA box (64-row tiles)
     (5, 2, 0): 1.0,    # c2s (5x5)
 }
 
@@ -41,6 +42,12 @@ def _scan():
         if m:
             kx, sh, ry, edge, pk = map(int, m.groups())
             key = (kx, sh, ry, edge, pk)
+            stats[key] = [0, 0]
+            continue
+        m = re.search(r"Function : \S*correlate_pair_kernelILi(\d+)ELi(\d)ELi(\d)E", line)
+        if m:  # two output planes per CTA (config 4's full tiles): key edge = -1
+            kx, sh, ry = map(int, m.groups())
+            key = (kx, sh, ry, -1, 0)
             stats[key] = [0, 0]
             continue
         if "Function :" in line:
@@ -70,4 +77,9 @@ def test_tap_operands_on_uniform_datapath():
             # steps of the Richardson-Lucy ratio's divisions, inlined or not as ptxas decides)
             if (u + min(t - u, EPILOGUE_FMAS)) / t < need:
                 bad.append(f"<{kx},{sh},{ry},0,{pk}>: {u}/{t} FMAs on uniform taps (need {need:.0%})")
+    for sh in (0, 2):  # config 4's two-planes kernel
+        t, u = stats.get((9, sh, 2, -1, 0), (0, 0))
+        assert t > 0, f"correlate_pair_kernel<9,{sh},2> not found in {N.LIB_PATH}"
+        if (u + min(t - u, EPILOGUE_FMAS)) / t < 1.0:
+            bad.append(f"pair<9,{sh},2>: {u}/{t} FMAs on uniform taps")
     assert not bad, "tap loop left the uniform datapath: " + "; ".join(bad)
