@@ -1,6 +1,7 @@
 #!/bin/bash
 # A/B kernel timing of library variants with SM clock / power sampled alongside.
-# usage: tools/ab_kbench.sh "c2 c2k3" lib_old lib_new ...   (libs under tools/variants/)
+# usage: tools/ab_kbench.sh "c2 c2k3" lib_old lib_new ...   (libs under tools/variants/;
+# tools/variants/ is listed in .gpurunignore -- remove that line while running A/Bs on the GPU box)
 CFGS=$1; shift
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=timestamp,clocks.sm,power.draw,clocks_throttle_reasons.active --format=csv -lms 200 \
