@@ -53,11 +53,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Named CTA barrier `id`, split into its two halves: the warps that only signal (arrive,
 // non-blocking) and the warp that waits for all `count` threads (sync).
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-  asm volatile("barrier.cta.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+template <int ID>
+__device__ __forceinline__ void bar_arrive() {
+  asm volatile("barrier.cta.arrive %0, %1;" ::"n"(ID), "n"(kThreads) : "memory");
 }
-__device__ __forceinline__ void bar_sync(int id, int count) {
-  asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+template <int ID>
+__device__ __forceinline__ void bar_sync() {
+  asm volatile("barrier.cta.sync %0, %1;" ::"n"(ID), "n"(kThreads) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -809,10 +811,14 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_of<KX, RY, EDGE, PK>()))
       // The full-tile kernels keep the plain barrier: with any split form ptxas moves
       // config 4's tap loads off the uniform datapath (profiles/r02e_tap_loop_probes.md).
       if constexpr (EDGE) {
-        if (warp != 0)
-          bar_arrive(1 + s, kThreads);
-        else
-          bar_sync(1 + s, kThreads);
+        // (literal barrier ids: with a register id ptxas reserves all 16 barriers per CTA)
+        if (s == 0) {
+          if (warp != 0) bar_arrive<1>(); else bar_sync<1>();
+        } else if (s == 1) {
+          if (warp != 0) bar_arrive<2>(); else bar_sync<2>();
+        } else {
+          if (warp != 0) bar_arrive<3>(); else bar_sync<3>();
+        }
       } else {
         __syncthreads();
       }
